@@ -1,0 +1,108 @@
+/*
+ * tokenring.h -- C ABI of libtokenring.so, the B200 (sm_100a) TokenRing
+ * attention path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * passed as void*; none of them allocates, synchronises the device or keeps
+ * state across calls (except tr_p2p_* which own a per-process peer table).
+ * All return TR_OK (0) or a negative status; the message of the last failure
+ * on the calling thread is available from tr_last_error().
+ *
+ * Tensor conventions (same as the reference, pkg/src/ringsim/core.py:5-7):
+ *   q, k, v, out : token-major (T, H, D), contiguous, bf16 unless stated
+ *   lse          : head-major  (H, T) float32, natural log, -inf = empty row
+ *
+ * Reference interfaces replaced (all paths relative to /root/reference):
+ *   tr_attention_block  <- kernels.attention_block   pkg/src/ringsim/kernels.py:39
+ *                          (_kernels_ref.py:34-54, _kernels.pyx:15-65)
+ *   tr_merge_state      <- kernels.merge_state       pkg/src/ringsim/kernels.py:40
+ *                          (_kernels_ref.py:66-73, _kernels.pyx:68-102)
+ *   tr_attention_segments  the per-step block computations of
+ *                          engine.execute pkg/src/ringsim/engine.py:558-593
+ *                          (several ComputePlans of one step in one launch)
+ *   tr_splitmix_bf16    <- rng.uniform / attention_inputs pkg/src/ringsim/rng.py:34-53
+ */
+#ifndef TOKENRING_H_
+#define TOKENRING_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python layer maps them onto ringsim's exception types
+ * (pkg/src/ringsim/errors.py:4-25). */
+#define TR_OK 0
+#define TR_ERR_DIMENSION -1   /* DimensionError */
+#define TR_ERR_INPUT -2       /* InputError */
+#define TR_ERR_CONFIG -3      /* ConfigError */
+#define TR_ERR_CUDA -4        /* CUDA runtime / driver failure */
+#define TR_ERR_UNSUPPORTED -5 /* shape the sm_100a kernels do not cover */
+
+/* mask kinds, identical to ringsim.kernels.MASK_* (pkg/src/ringsim/kernels.py:33-35) */
+#define TR_MASK_NONE 0
+#define TR_MASK_FULL 1
+#define TR_MASK_CAUSAL 2
+
+/* dtypes for merge operands */
+#define TR_DTYPE_F32 0
+#define TR_DTYPE_BF16 1
+
+/* One contiguous run of tokens inside a local (T, H, D) buffer:
+ * local rows [row0, row0 + rows) sit at global sequence positions
+ * [pos0, pos0 + rows).  Causal visibility is decided on positions:
+ * key j is visible to query i iff pos(i) >= pos(j)  (ref _kernels_ref.py:42-44). */
+typedef struct tr_segment {
+  int64_t row0;
+  int64_t rows;
+  int64_t pos0;
+} tr_segment;
+
+#define TR_MAX_SEGMENTS 4
+
+/* kernels.attention_block: out (tq,H,D) bf16, lse (H,tq) f32 for one q block
+ * against one kv block.  mask_kind FULL writes the identity (0 / -inf)
+ * without reading q/k/v.  CAUSAL uses q_offset/k_offset as global positions. */
+int tr_attention_block(const void* q, const void* k, const void* v, void* out, float* lse,
+                       int64_t tq, int64_t tk, int32_t heads, int32_t head_dim,
+                       int32_t mask_kind, int64_t q_offset, int64_t k_offset, void* stream);
+
+/* Several q segments of one local q buffer against several kv segments of one
+ * local k/v buffer, in one launch.  Every q segment attends to the union of the
+ * kv segments (causal: by position).  out/lse rows follow q's local rows;
+ * lse has row stride tq_total.  Rows of q not covered by a segment are left
+ * untouched. */
+int tr_attention_segments(const void* q, const void* k, const void* v, void* out, float* lse,
+                          int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
+                          const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
+                          int32_t n_kv, int32_t causal, void* stream);
+
+/* kernels.merge_state, in place on a float32 accumulator:
+ *   acc <- merge(acc, blk)     (ref _kernels.pyx:68-102)
+ * blk_out is bf16 or f32 (blk_dtype); -inf rows are exact identities.
+ * If final_out != NULL the merged output is also written there as bf16. */
+int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t blk_dtype,
+                   const float* blk_lse, int64_t tokens, int32_t heads, int32_t head_dim,
+                   int64_t acc_lse_stride, int64_t blk_lse_stride, void* final_out,
+                   void* stream);
+
+/* Identity accumulator (Partial.empty, ref core.py:75-78): out = 0, lse = -inf. */
+int tr_partial_init(float* acc_out, float* acc_lse, int64_t tokens, int32_t heads,
+                    int32_t head_dim, void* stream);
+
+/* SplitMix64 draws [first, first+count) of `seed` mapped to uniform
+ * [low, high) in float64 exactly as rng.uniform, then rounded
+ * fp64 -> fp32 -> bf16 (RNE).  dst receives `count` bf16 values. */
+int tr_splitmix_bf16(uint64_t seed, int64_t first, int64_t count, double low, double high,
+                     void* dst, void* stream);
+
+/* Version / capability probes (no GPU work). */
+const char* tr_version(void);
+int32_t tr_kernel_count(void);
+const char* tr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOKENRING_H_ */

@@ -1,0 +1,100 @@
+"""ctypes binding of libtokenring.so (the C ABI declared in include/tokenring.h).
+
+The library is built in-tree (``python -m paper_2412_20501_b200.build``).  There
+is no fallback: if the shared object is missing or fails to load, every
+compute entry point raises -- the product path never silently degrades to a
+CPU or PyTorch implementation.
+"""
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigError, DimensionError, InputError, RingsimError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtokenring.so")
+
+TR_OK = 0
+TR_ERR_DIMENSION = -1
+TR_ERR_INPUT = -2
+TR_ERR_CONFIG = -3
+TR_ERR_CUDA = -4
+TR_ERR_UNSUPPORTED = -5
+
+TR_DTYPE_F32 = 0
+TR_DTYPE_BF16 = 1
+
+# every symbol include/tokenring.h declares
+EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_merge_state", "tr_partial_init",
+           "tr_splitmix_bf16", "tr_version", "tr_kernel_count", "tr_last_error")
+
+
+class CudaError(RingsimError, RuntimeError):
+    """A CUDA runtime/driver call inside libtokenring failed."""
+
+
+class UnsupportedError(RingsimError, ValueError):
+    """The sm_100a kernels do not cover this shape."""
+
+
+class Segment(ctypes.Structure):
+    """tr_segment: local rows [row0, row0+rows) at global positions pos0.."""
+    _fields_ = [("row0", ctypes.c_int64), ("rows", ctypes.c_int64), ("pos0", ctypes.c_int64)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(lib):
+    i64, i32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    lib.tr_attention_block.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i64, i64, vp]
+    lib.tr_attention_segments.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32,
+                                          ctypes.POINTER(Segment), i32,
+                                          ctypes.POINTER(Segment), i32, i32, vp]
+    lib.tr_merge_state.argtypes = [vp, vp, vp, i32, vp, i64, i32, i32, i64, i64, vp, vp]
+    lib.tr_partial_init.argtypes = [vp, vp, i64, i32, i32, vp]
+    lib.tr_splitmix_bf16.argtypes = [ctypes.c_uint64, i64, i64, ctypes.c_double,
+                                     ctypes.c_double, vp, vp]
+    for name in ("tr_attention_block", "tr_attention_segments", "tr_merge_state",
+                 "tr_partial_init", "tr_splitmix_bf16"):
+        getattr(lib, name).restype = ctypes.c_int
+    lib.tr_version.restype = ctypes.c_char_p
+    lib.tr_version.argtypes = []
+    lib.tr_kernel_count.restype = ctypes.c_int32
+    lib.tr_kernel_count.argtypes = []
+    lib.tr_last_error.restype = ctypes.c_char_p
+    lib.tr_last_error.argtypes = []
+
+
+def lib():
+    """Load (once) and return the ctypes handle; raises if it is not built."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(
+                        f"{LIB_PATH} is not built; run `python -m paper_2412_20501_b200.build` "
+                        "(there is no CPU fallback)")
+                handle = ctypes.CDLL(LIB_PATH)
+                _declare(handle)
+                _lib = handle
+    return _lib
+
+
+def check(status):
+    """Map a TR_* status onto the reference's exception taxonomy (errors.py:4-25)."""
+    if status == TR_OK:
+        return
+    msg = lib().tr_last_error().decode(errors="replace")
+    if status == TR_ERR_DIMENSION:
+        raise DimensionError(msg)
+    if status == TR_ERR_INPUT:
+        raise InputError(msg)
+    if status == TR_ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == TR_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    raise CudaError(msg)

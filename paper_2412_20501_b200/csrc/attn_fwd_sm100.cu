@@ -1,0 +1,411 @@
+// Block attention forward for sm_100a: tcgen05 MMA with TMEM accumulators,
+// TMA-staged Q/K/V tiles (128-byte swizzle), warp-specialised CTA.
+//
+// Computes, for every (q row i, head h) of the q segments against the union
+// of the kv segments (ref _kernels_ref.py:34-54, _kernels.pyx:15-65):
+//     lse(h,i) = log sum_j exp(s_ij),   out(i,h) = sum_j softmax(s)_ij v_j,
+//     s_ij = q_i . k_j / sqrt(D),   causal: j visible iff pos(i) >= pos(j),
+// rows without visible keys -> lse = -inf, out = 0.
+//
+// CTA = one head x 256 query rows (two 128-row tiles, "halves").
+//   warp 0      TMA producer: Q once, then K_j / V_j into an NS-stage ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 4-7   softmax + epilogue for half 0   (TMEM lanes 0..127)
+//   warps 8-11  softmax + epilogue for half 1
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D);
+// P_h (bf16, packed 2/col) overwrites S_h columns [0,64) once S_h is in
+// registers, and is the A operand of the P.V MMA straight from TMEM.
+// MMA issue order per kv tile j (keeps the tensor pipe busy while the two
+// softmax groups alternate):  S0=Q0.Kj | O1+=P1.V(j-1) | S1=Q1.Kj | O0+=P0.Vj
+// Online softmax keeps a stale running max unless it grows by > 8 (log2
+// units): exact rescaling, done rarely, by the softmax warps themselves while
+// the O accumulator is quiescent.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cmath>
+#include <mutex>
+
+#include "tr_internal.h"
+#include "tr_ptx.cuh"
+
+namespace tr {
+
+template <int D>
+struct AttnCfg {
+  static constexpr int BM = 128;  // rows per half
+  static constexpr int BN = 128;  // keys per kv tile
+  static constexpr int NB = D / 64;               // 64-column TMA boxes per tile row
+  static constexpr int BOX = 128 * 64 * 2;        // bytes per box (16 KB)
+  static constexpr int TILE = NB * BOX;           // bytes per 128-row tile
+  static constexpr int NS = (D == 128) ? 4 : 6;   // kv ring stages (K and V alternate)
+  static constexpr int THREADS = 384;
+  static constexpr int SMEM_TILES = (2 + NS) * TILE;
+  static constexpr int SMEM = SMEM_TILES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+  static constexpr uint32_t IDESC_QK = idesc_bf16(128, BN, false);
+  static constexpr uint32_t IDESC_PV = idesc_bf16(128, D, true);
+  static constexpr float RESCALE_LOG2 = 8.0f;
+};
+
+struct KvCursor {
+  int64_t tiles[TR_MAX_SEGMENTS];
+  int total;
+};
+
+__device__ __forceinline__ void q_tile_of(const AttnPlan& p, int64_t lin, int& seg, int64_t& row0) {
+  seg = 0;
+  while (seg + 1 < p.nq && lin >= p.tile_prefix[seg + 1]) ++seg;
+  int64_t local = lin - p.tile_prefix[seg];
+  if (p.causal) local = (p.tile_prefix[seg + 1] - p.tile_prefix[seg]) - 1 - local;  // heavy first
+  row0 = local * 256;
+}
+
+__device__ __forceinline__ KvCursor kv_tiles_for(const AttnPlan& p, int64_t qmax_pos) {
+  KvCursor c;
+  c.total = 0;
+  for (int g = 0; g < TR_MAX_SEGMENTS; ++g) {
+    int64_t n = 0;
+    if (g < p.nkv) {
+      n = (p.kv[g].rows + 127) / 128;
+      if (p.causal) {
+        if (qmax_pos < p.kv[g].pos0) n = 0;
+        else n = min(n, (qmax_pos - p.kv[g].pos0) / 128 + 1);
+      }
+    }
+    c.tiles[g] = n;
+    c.total += static_cast<int>(n);
+  }
+  return c;
+}
+
+// j-th kv tile of the cursor -> (local row of its first key, position, valid keys)
+__device__ __forceinline__ void kv_tile_at(const AttnPlan& p, const KvCursor& c, int j,
+                                           int64_t& row, int64_t& pos, int& valid) {
+  int g = 0;
+  int64_t t = j;
+  while (t >= c.tiles[g]) { t -= c.tiles[g]; ++g; }
+  row = p.kv[g].row0 + t * 128;
+  pos = p.kv[g].pos0 + t * 128;
+  valid = static_cast<int>(imin64(128, p.kv[g].rows - t * 128));
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+                      const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnPlan p) {
+  using C = AttnCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                      // 2 tiles
+  uint8_t* sKV = smem + 2 * C::TILE;       // NS tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_TILES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;                 // [NS]
+  uint64_t* kv_empty = bars + 1 + C::NS;        // [NS]
+  uint64_t* s_full = bars + 1 + 2 * C::NS;      // [2]
+  uint64_t* p_full = bars + 3 + 2 * C::NS;      // [2]
+  uint64_t* o_done = bars + 5 + 2 * C::NS;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * C::NS);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int head = static_cast<int>(blockIdx.x / p.tile_prefix[p.nq]);
+  const int64_t lin = blockIdx.x % p.tile_prefix[p.nq];
+  int qseg;
+  int64_t qrow0;  // first row of this CTA inside its q segment
+  q_tile_of(p, lin, qseg, qrow0);
+  const tr_segment Q = p.q[qseg];
+  const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
+  const KvCursor kvc = kv_tiles_for(p, qmax_pos);
+  const int ntiles = kvc.total;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int h = 0; h < 2; ++h) { mbar_init(&s_full[h], 1); mbar_init(&p_full[h], 128); mbar_init(&o_done[h], 1); }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmq); tma_prefetch_desc(&tmk); tma_prefetch_desc(&tmv);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0 && ntiles > 0) {
+      const int32_t col0 = head * D;
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE);
+      for (int h = 0; h < 2; ++h)
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d(sQ + (h * C::NB + b) * C::BOX, &tmq, q_full, col0 + 64 * b,
+                      static_cast<int32_t>(Q.row0 + qrow0 + 128 * h), kEvictFirst);
+      int n = 0;
+      for (int j = 0; j < ntiles; ++j) {
+        int64_t krow, kpos;
+        int valid;
+        kv_tile_at(p, kvc, j, krow, kpos, valid);
+        for (int which = 0; which < 2; ++which, ++n) {
+          const int s = n % C::NS;
+          const uint32_t round = n / C::NS;
+          mbar_wait(&kv_empty[s], (round & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[s], C::TILE);
+          const CUtensorMap* tm = which ? &tmv : &tmk;
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b,
+                        static_cast<int32_t>(krow), kEvictLast);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      const uint32_t tS[2] = {tmem + 0, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const uint32_t q_addr = smem_u32(sQ);
+      const uint32_t kv_addr = smem_u32(sKV);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto qk = [&](int h, int stage) {
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * C::BOX + (kk % 4) * 32;
+          const uint64_t a = sdesc_sw128(q_addr + h * C::TILE + off, 16, 1024);
+          const uint64_t b = sdesc_sw128(kv_addr + stage * C::TILE + off, 16, 1024);
+          mma_ss(tS[h], a, b, C::IDESC_QK, kk > 0);
+        }
+      };
+      auto pv = [&](int h, int stage, bool acc) {
+        for (int kk = 0; kk < C::BN / 16; ++kk) {
+          const uint64_t b = sdesc_sw128(kv_addr + stage * C::TILE + kk * 2048, C::BOX, 1024);
+          mma_ts(tO[h], tS[h] + kk * 8, b, C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      int prev_v_stage = 0;
+      for (int j = 0; j < ntiles; ++j) {
+        const int nk = 2 * j, nv = 2 * j + 1;
+        const int sk = nk % C::NS, sv = nv % C::NS;
+        mbar_wait(&kv_full[sk], (nk / C::NS) & 1);
+        tc_fence_after();
+        qk(0, sk);
+        tc_commit(&s_full[0]);
+        if (j > 0) {
+          mbar_wait(&p_full[1], (j - 1) & 1);
+          tc_fence_after();
+          pv(1, prev_v_stage, j - 1 > 0);
+          tc_commit(&kv_empty[prev_v_stage]);
+        }
+        qk(1, sk);
+        tc_commit(&s_full[1]);
+        tc_commit(&kv_empty[sk]);
+        mbar_wait(&kv_full[sv], (nv / C::NS) & 1);
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        pv(0, sv, j > 0);
+        if (j == ntiles - 1) tc_commit(&o_done[0]);
+        prev_v_stage = sv;
+      }
+      mbar_wait(&p_full[1], (ntiles - 1) & 1);
+      tc_fence_after();
+      pv(1, prev_v_stage, ntiles - 1 > 0);
+      tc_commit(&kv_empty[prev_v_stage]);
+      tc_commit(&o_done[1]);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int h = (warp - 4) / 4;         // which 128-row half
+    const int quarter = warp % 4;         // TMEM lane quarter
+    const int r = quarter * 32 + lane;    // row inside the half
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + h * 128;
+    const uint32_t tO = tmem + lane_base + 256 + h * 128;
+    const int64_t row_in_seg = qrow0 + 128 * h + r;
+    const int64_t my_pos = Q.pos0 + row_in_seg;
+    const int64_t half_min_pos = Q.pos0 + qrow0 + 128 * h;
+    const float c = p.scale_log2;
+    const float thresh = C::RESCALE_LOG2 / c;
+    float m_used = -INFINITY;
+    float l = 0.f;
+    for (int j = 0; j < ntiles; ++j) {
+      int64_t krow, kpos;
+      int valid;
+      kv_tile_at(p, kvc, j, krow, kpos, valid);
+      mbar_wait(&s_full[h], j & 1);
+      tc_fence_after();
+      float s[128];
+      #pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t u[32];
+        tmem_ld32(tS + cc * 32, u);
+        tc_wait_ld();
+        #pragma unroll
+        for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(u[i]);
+      }
+      const bool need_mask = valid < 128 || (p.causal && kpos + 127 > half_min_pos);
+      if (need_mask) {
+        int64_t lim = valid;
+        if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
+        const int limit = static_cast<int>(imax64(lim, 0));
+        #pragma unroll
+        for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : -INFINITY;
+      }
+      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+      #pragma unroll
+      for (int i = 4; i < 128; i += 4) {
+        mx0 = fmaxf(mx0, s[i]); mx1 = fmaxf(mx1, s[i + 1]);
+        mx2 = fmaxf(mx2, s[i + 2]); mx3 = fmaxf(mx3, s[i + 3]);
+      }
+      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+      const bool grow = mx > m_used + thresh;
+      const bool scale_o = grow && m_used != -INFINITY;
+      // tcgen05.ld/st are warp-collective: decide per warp, scale per row.
+      if (__any_sync(0xffffffffu, scale_o)) {
+        // O holds only completed P.V products (this tile's S commit implies
+        // every earlier MMA finished); rescale it before publishing P_j.
+        const float f = scale_o ? ex2_approx((m_used - mx) * c) : 1.f;
+        l *= f;
+        #pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t u[32];
+          tmem_ld32(tO + cc * 32, u);
+          tc_wait_ld();
+          #pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * f);
+          tmem_st32(tO + cc * 32, u);
+        }
+      }
+      if (grow) m_used = mx;
+      const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
+      float l0 = 0.f, l1 = 0.f;
+      #pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t pk[32];
+        #pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float a = ex2_approx(fmaf(s[cc * 64 + 2 * i], c, -mc));
+          const float b = ex2_approx(fmaf(s[cc * 64 + 2 * i + 1], c, -mc));
+          l0 += a;
+          l1 += b;
+          pk[i] = pack_bf16x2(a, b);
+        }
+        tmem_st32(tS + cc * 32, pk);
+      }
+      l += l0 + l1;
+      tc_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[h]);
+    }
+    // ---------------------------------------------------------- epilogue
+    const bool row_ok = row_in_seg < Q.rows;
+    const int64_t grow = Q.row0 + row_in_seg;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow * p.heads + head) * D;
+    if (ntiles > 0) {
+      mbar_wait(&o_done[h], 0);
+      tc_fence_after();
+    }
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    #pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t u[32];
+      if (ntiles > 0) {
+        tmem_ld32(tO + cc * 32, u);
+        tc_wait_ld();
+      } else {
+        #pragma unroll
+        for (int i = 0; i < 32; ++i) u[i] = 0u;
+      }
+      uint32_t pk[16];
+      #pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(__uint_as_float(u[2 * i]) * inv, __uint_as_float(u[2 * i + 1]) * inv);
+      if (row_ok) {
+        uint4* dst = reinterpret_cast<uint4*>(out + cc * 32);
+        #pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+    if (row_ok)
+      p.lse[head * p.lse_stride + grow] = (l > 0.f) ? (logf(l) + m_used * p.scale) : -INFINITY;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+static int make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t row_elems) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(TR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_elems), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * 2)};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TR_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return TR_OK;
+}
+
+bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const void* v,
+                    const void* out) {
+  if (head_dim != 64 && head_dim != 128) return false;
+  const int64_t row_bytes = int64_t(heads) * head_dim * 2;
+  if (row_bytes % 16) return false;
+  for (const void* ptr : {q, k, v, out})
+    if (reinterpret_cast<uintptr_t>(ptr) % 16) return false;
+  return true;
+}
+
+template <int D>
+static int launch_d(const void* q, const void* k, const void* v, int64_t tq_total, int64_t tk_total,
+                    AttnPlan& plan, cudaStream_t s) {
+  using C = AttnCfg<D>;
+  CUtensorMap tq, tk, tv;
+  const int64_t row_elems = int64_t(plan.heads) * D;
+  int rc;
+  if ((rc = make_tmap(&tq, q, tq_total, row_elems))) return rc;
+  if ((rc = make_tmap(&tk, k, tk_total, row_elems))) return rc;
+  if ((rc = make_tmap(&tv, v, tk_total, row_elems))) return rc;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_sm100)");
+    attr_done = true;
+  }
+  const int64_t blocks = plan.tile_prefix[plan.nq] * plan.heads;
+  if (blocks == 0) return TR_OK;
+  if (blocks > 0x7FFFFFFF) return fail(TR_ERR_UNSUPPORTED, "grid too large");
+  attn_fwd_sm100_kernel<D><<<static_cast<unsigned>(blocks), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
+  return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
+}
+
+int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_total,
+                      int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s) {
+  if (head_dim == 128) return launch_d<128>(q, k, v, tq_total, tk_total, plan, s);
+  if (head_dim == 64) return launch_d<64>(q, k, v, tq_total, tk_total, plan, s);
+  return fail(TR_ERR_UNSUPPORTED, "sm100 attention kernel supports head_dim 64 or 128");
+}
+
+}  // namespace tr

@@ -1,0 +1,138 @@
+// extern "C" boundary of libtokenring.so (see include/tokenring.h).
+// Validation mirrors the reference's Python-side checks
+// (core.py:96-119 DimensionError, partition.py:59-62 ConfigError) so the
+// Python wrapper can map status codes onto the same exception classes.
+#include <cuda_runtime.h>
+#include <cmath>
+#include <string>
+
+#include "tr_internal.h"
+
+namespace tr {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return TR_OK;
+  return fail(TR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int launch_merge(float* acc_out, float* acc_lse, const void* blk_out, int blk_dtype,
+                 const float* blk_lse, int64_t T, int H, int D, int64_t als, int64_t bls,
+                 void* fin, cudaStream_t s);
+int launch_partial_init(float* acc_out, float* acc_lse, int64_t T, int H, int D, cudaStream_t s);
+int launch_fill(float* p, int64_t n, float v, cudaStream_t s);
+int launch_splitmix(uint64_t seed, int64_t first, int64_t count, double low, double high,
+                    void* dst, cudaStream_t s);
+
+static int check_segments(const tr_segment* segs, int n, int64_t total, const char* what) {
+  if (n < 0 || n > TR_MAX_SEGMENTS)
+    return fail(TR_ERR_CONFIG, std::string(what) + ": segment count must be in [0, 4]");
+  for (int i = 0; i < n; ++i) {
+    if (segs[i].rows < 0 || segs[i].row0 < 0 || segs[i].row0 + segs[i].rows > total)
+      return fail(TR_ERR_DIMENSION, std::string(what) + ": segment outside the buffer");
+  }
+  return TR_OK;
+}
+
+static int run_segments(const void* q, const void* k, const void* v, void* out, float* lse,
+                        int64_t tq_total, int64_t tk_total, int heads, int head_dim,
+                        const tr_segment* qs, int nq, const tr_segment* ks, int nk, int causal,
+                        cudaStream_t s) {
+  if (heads < 1 || head_dim < 1 || tq_total < 0 || tk_total < 0)
+    return fail(TR_ERR_DIMENSION, "heads, head_dim must be >= 1 and token counts >= 0");
+  int rc;
+  if ((rc = check_segments(qs, nq, tq_total, "q"))) return rc;
+  if ((rc = check_segments(ks, nk, tk_total, "kv"))) return rc;
+  AttnPlan plan{};
+  plan.nq = 0;
+  for (int i = 0; i < nq; ++i)
+    if (qs[i].rows > 0) plan.q[plan.nq++] = qs[i];
+  plan.nkv = 0;
+  for (int i = 0; i < nk; ++i)
+    if (ks[i].rows > 0) plan.kv[plan.nkv++] = ks[i];
+  if (plan.nq == 0) return TR_OK;
+  plan.causal = causal ? 1 : 0;
+  plan.heads = heads;
+  plan.lse_stride = tq_total;
+  plan.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(head_dim)));
+  plan.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(head_dim)));
+  plan.out = out;
+  plan.lse = lse;
+  plan.tile_prefix[0] = 0;
+  for (int i = 0; i < plan.nq; ++i)
+    plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
+  if (sm100_supports(head_dim, heads, q, k, v, out) && plan.nkv > 0)
+    return launch_attn_sm100(q, k, v, tq_total, tk_total, head_dim, plan, s);
+  return launch_attn_simt(q, k, v, head_dim, plan, s);
+}
+
+}  // namespace tr
+
+using namespace tr;
+
+extern "C" {
+
+int tr_attention_block(const void* q, const void* k, const void* v, void* out, float* lse,
+                       int64_t tq, int64_t tk, int32_t heads, int32_t head_dim, int32_t mask_kind,
+                       int64_t q_offset, int64_t k_offset, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (mask_kind != TR_MASK_NONE && mask_kind != TR_MASK_FULL && mask_kind != TR_MASK_CAUSAL)
+    return fail(TR_ERR_CONFIG, "mask_kind must be 0 (none), 1 (full) or 2 (causal)");
+  if (heads < 1 || head_dim < 1 || tq < 0 || tk < 0)
+    return fail(TR_ERR_DIMENSION, "tq, tk >= 0 and heads, head_dim >= 1 required");
+  if (mask_kind == TR_MASK_FULL || tk == 0) {
+    // identity rows without reading the inputs (ref _kernels_ref.py:37-38)
+    int rc = cuda_status(cudaMemsetAsync(out, 0, size_t(tq) * heads * head_dim * 2, s), "memset out");
+    if (rc) return rc;
+    return launch_fill(lse, tq * heads, -INFINITY, s);
+  }
+  tr_segment qs{0, tq, q_offset};
+  tr_segment ks{0, tk, k_offset};
+  return run_segments(q, k, v, out, lse, tq, tk, heads, head_dim, &qs, 1, &ks, 1,
+                      mask_kind == TR_MASK_CAUSAL, s);
+}
+
+int tr_attention_segments(const void* q, const void* k, const void* v, void* out, float* lse,
+                          int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
+                          const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
+                          int32_t n_kv, int32_t causal, void* stream) {
+  return run_segments(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
+                      n_kv, causal, static_cast<cudaStream_t>(stream));
+}
+
+int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t blk_dtype,
+                   const float* blk_lse, int64_t tokens, int32_t heads, int32_t head_dim,
+                   int64_t acc_lse_stride, int64_t blk_lse_stride, void* final_out, void* stream) {
+  if (tokens < 0 || heads < 1 || head_dim < 1)
+    return fail(TR_ERR_DIMENSION, "tokens >= 0, heads >= 1, head_dim >= 1 required");
+  if (acc_lse_stride < tokens || blk_lse_stride < tokens)
+    return fail(TR_ERR_DIMENSION, "lse row stride smaller than the token count");
+  return launch_merge(acc_out, acc_lse, blk_out, blk_dtype, blk_lse, tokens, heads, head_dim,
+                      acc_lse_stride, blk_lse_stride, final_out, static_cast<cudaStream_t>(stream));
+}
+
+int tr_partial_init(float* acc_out, float* acc_lse, int64_t tokens, int32_t heads,
+                    int32_t head_dim, void* stream) {
+  if (tokens < 0 || heads < 1 || head_dim < 1)
+    return fail(TR_ERR_DIMENSION, "tokens >= 0, heads >= 1, head_dim >= 1 required");
+  return launch_partial_init(acc_out, acc_lse, tokens, heads, head_dim,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int tr_splitmix_bf16(uint64_t seed, int64_t first, int64_t count, double low, double high,
+                     void* dst, void* stream) {
+  if (first < 0 || count < 0) return fail(TR_ERR_CONFIG, "first and count must be >= 0");
+  return launch_splitmix(seed, first, count, low, high, dst, static_cast<cudaStream_t>(stream));
+}
+
+const char* tr_version(void) { return "tokenring-b200 0.1 (sm_100a)"; }
+int32_t tr_kernel_count(void) { return 7; }
+const char* tr_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

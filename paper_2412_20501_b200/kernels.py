@@ -1,0 +1,145 @@
+"""Kernel boundary: the two primitives of ``ringsim.kernels``
+(``pkg/src/ringsim/kernels.py:33-40``) on CUDA tensors, executed by the
+sm_100a kernels of libtokenring.so through its C ABI.
+
+``attention_block(q, k, v, mask_kind, q_offset, k_offset) -> (out, lse)``
+    q (Tq,H,D), k/v (Tk,H,D) bf16 CUDA tensors -> out (Tq,H,D) bf16,
+    lse (H,Tq) float32 (ref ``_kernels_ref.py:34-54``).
+``merge_state(acc_out, acc_lse, blk_out, blk_lse) -> (out, lse)``
+    returns a new float32 accumulator (ref ``_kernels_ref.py:66-73``);
+    ``merge_state_`` is the in-place form the executors use.
+
+Unlike the reference there is exactly one backend: ``BACKEND`` names it and
+there is no environment switch and no CPU fallback.
+"""
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import DimensionError
+
+MASK_NONE = 0
+MASK_FULL = 1
+MASK_CAUSAL = 2
+
+BACKEND = "cuda-sm100a"
+
+
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _require_cuda(name, t, dtype=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise DimensionError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise DimensionError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise DimensionError(f"{name} must be contiguous")
+
+
+def _check_qkv(q, k, v):
+    for n, t in (("q", q), ("k", k), ("v", v)):
+        _require_cuda(n, t, torch.bfloat16)
+        if t.dim() != 3:
+            raise DimensionError(f"{n} must have shape (T, H, D), got {tuple(t.shape)}")
+    if q.shape[1] != k.shape[1] or q.shape[1] != v.shape[1]:
+        raise DimensionError(f"head counts differ: q={q.shape[1]} k={k.shape[1]} v={v.shape[1]}")
+    if q.shape[2] != k.shape[2] or q.shape[2] != v.shape[2]:
+        raise DimensionError(f"head dims differ: q={q.shape[2]} k={k.shape[2]} v={v.shape[2]}")
+    if k.shape[0] != v.shape[0]:
+        raise DimensionError(f"k has {k.shape[0]} tokens but v has {v.shape[0]}")
+
+
+def attention_block(q, k, v, mask_kind=MASK_NONE, q_offset=0, k_offset=0, out=None, lse=None):
+    _check_qkv(q, k, v)
+    tq, h, d = q.shape
+    tk = k.shape[0]
+    if out is None:
+        out = torch.empty((tq, h, d), dtype=torch.bfloat16, device=q.device)
+    if lse is None:
+        lse = torch.empty((h, tq), dtype=torch.float32, device=q.device)
+    _require_cuda("out", out, torch.bfloat16)
+    _require_cuda("lse", lse, torch.float32)
+    _lib.check(_lib.lib().tr_attention_block(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), tq, tk, h, d, int(mask_kind),
+        int(q_offset), int(k_offset), _stream(q.device)))
+    return out, lse
+
+
+def _segs(segs):
+    arr = (_lib.Segment * max(1, len(segs)))()
+    for i, (row0, rows, pos0) in enumerate(segs):
+        arr[i] = _lib.Segment(int(row0), int(rows), int(pos0))
+    return arr
+
+
+def attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse):
+    """Every q segment (row0, rows, pos0) against the union of the kv segments
+    in one launch; writes out/lse rows of the q segments only."""
+    _check_qkv(q, k, v)
+    _require_cuda("out", out, torch.bfloat16)
+    _require_cuda("lse", lse, torch.float32)
+    if out.shape != q.shape or lse.shape != (q.shape[1], q.shape[0]):
+        raise DimensionError("out/lse must match q's (T,H,D) / (H,T)")
+    qs, ks = _segs(q_segs), _segs(kv_segs)
+    _lib.check(_lib.lib().tr_attention_segments(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
+        q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, _stream(q.device)))
+    return out, lse
+
+
+def merge_state_(acc_out, acc_lse, blk_out, blk_lse, final_out=None):
+    """In place: acc <- merge(acc, blk).  acc_out float32 (T,H,D); acc_lse /
+    blk_lse may be column slices of wider (H, S) buffers (row stride S)."""
+    _require_cuda("acc_out", acc_out, torch.float32)
+    if not isinstance(blk_out, torch.Tensor) or not blk_out.is_cuda or not blk_out.is_contiguous():
+        raise DimensionError("blk_out must be a contiguous CUDA tensor")
+    if blk_out.dtype not in (torch.bfloat16, torch.float32):
+        raise DimensionError("blk_out must be bf16 or float32")
+    if acc_out.shape != blk_out.shape:
+        raise DimensionError(
+            f"cannot merge partials of shape {tuple(acc_out.shape)} and {tuple(blk_out.shape)}")
+    t, h, d = acc_out.shape
+    for n, l in (("acc_lse", acc_lse), ("blk_lse", blk_lse)):
+        if l.dtype != torch.float32 or l.shape != (h, t) or l.stride(1) != 1:
+            raise DimensionError(f"{n} must be float32 (H, T) with unit column stride")
+    dt = _lib.TR_DTYPE_BF16 if blk_out.dtype == torch.bfloat16 else _lib.TR_DTYPE_F32
+    fin = None
+    if final_out is not None:
+        _require_cuda("final_out", final_out, torch.bfloat16)
+        fin = _ptr(final_out)
+    _lib.check(_lib.lib().tr_merge_state(
+        _ptr(acc_out), _ptr(acc_lse), _ptr(blk_out), dt, _ptr(blk_lse), t, h, d,
+        acc_lse.stride(0), blk_lse.stride(0), fin, _stream(acc_out.device)))
+    return acc_out, acc_lse
+
+
+def merge_state(acc_out, acc_lse, blk_out, blk_lse):
+    out = acc_out.to(torch.float32, copy=True).contiguous()
+    lse = acc_lse.to(torch.float32, copy=True).contiguous()
+    return merge_state_(out, lse, blk_out.contiguous(), blk_lse.to(torch.float32).contiguous())
+
+
+def partial_init_(acc_out, acc_lse):
+    _require_cuda("acc_out", acc_out, torch.float32)
+    _require_cuda("acc_lse", acc_lse, torch.float32)
+    t, h, d = acc_out.shape
+    _lib.check(_lib.lib().tr_partial_init(_ptr(acc_out), _ptr(acc_lse), t, h, d,
+                                          _stream(acc_out.device)))
+    return acc_out, acc_lse
+
+
+def splitmix_bf16_(dst, seed, first, low=-1.0, high=1.0):
+    """Fill contiguous bf16 ``dst`` with SplitMix64 draws first.. of ``seed``."""
+    _require_cuda("dst", dst, torch.bfloat16)
+    _lib.check(_lib.lib().tr_splitmix_bf16(
+        ctypes.c_uint64(int(seed) % (1 << 64)), int(first), dst.numel(), float(low), float(high),
+        _ptr(dst), _stream(dst.device)))
+    return dst
