@@ -1,0 +1,384 @@
+"""Benchmark of the TokenRing attention path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--seq S] [--impl reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (BASELINE.json configs[2], the metric's own config): zigzag
+TokenRing forward, S=131072 tokens, 32 heads, d=128, causal, bf16, over N
+ranks (strong scaling: the whole sequence is fixed, every rank owns S/N
+tokens).  At N=1 the schedule is the reference's trivial single-rank one
+(one causal block over the whole sequence, ref engine.py:176-184).
+
+A step = one full TokenRing forward (all P steps + final phase).  ``value``
+is whole-job algorithmic TFLOP/s (4*H*D*S(S+1)/2 per step, ref
+engine.py:170-173) over the max-over-ranks device time with inputs resident
+in HBM; ``e2e`` repeats the measurement through the same public API with the
+inputs copied from pinned host memory and the output copied back inside the
+timed region.  Every q/k/v tensor is 1 GiB (> 126 MB L2), so no explicit L2
+flush is needed between steps.
+
+``--impl reference`` times the reference's own CPU kernels (oracle/_ref:
+ringsim/_kernels.pyx compiled from the reference sources, or the numpy port
+in oracle/ when it is absent) on the host cores on a bounded sample of the
+same workload and prints the same JSON line with "impl": "reference".
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("Attention TFLOP/s + tokens/s at 128K seq on 1/2/4/8 B200; exposed comm ms/step")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--seq", type=int, default=131072)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--head-dim", type=int, default=128)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def causal_flops(S, H, D):
+    return 4 * H * D * (S * (S + 1) // 2)
+
+
+def workload_config(a, n):
+    return {"workload": f"zigzag TokenRing fwd, S={a.seq}, H={a.heads}, D={a.head_dim}, causal, "
+                        f"bf16, {n} rank(s)",
+            "seq_len": a.seq, "heads": a.heads, "head_dim": a.head_dim, "ranks": n,
+            "schedule": "zigzag-token-ring" if n > 1 else "zigzag-token-ring (P=1 trivial)",
+            "global_batch": 1, "parallelism": f"sp{n}",
+            "l2": "inputs larger than L2 (each q/k/v tensor >= 1 GiB at S=131072), no flush"}
+
+
+# ------------------------------------------------------------------ CPU side
+def _cpu_sample_worker(args):
+    """One worker: causal row windows of one head (rows at the end of the
+    sequence, keys 0..S) through the CPU kernels until ``budget`` seconds of
+    work are done.  Returns (algorithmic flops, seconds, rows)."""
+    kind, S, D, budget, seed = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    w = 8 if kind == "reference" else 128          # rows per call (bounded memory)
+    k = rng.uniform(-1, 1, (S, 1, D))
+    v = rng.uniform(-1, 1, (S, 1, D))
+    if kind == "reference":
+        from oracle import ref_kernels
+        mod = ref_kernels.load()
+
+        def call(q, a0):
+            mod.attention_block(q, k, v, 2, a0, 0)
+    else:
+        from oracle import kernels as ok
+
+        def call(q, a0):
+            ok.attention_block(q, k, v, ok.MASK_CAUSAL, a0, 0)
+    flops, rows, t0 = 0, 0, time.perf_counter()
+    while True:
+        a0 = S - w - (rows % (S // 2))
+        q = np.ascontiguousarray(rng.uniform(-1, 1, (w, 1, D)))
+        call(q, a0)
+        flops += 4 * D * (w * a0 + w * (w + 1) // 2)
+        rows += w
+        dt = time.perf_counter() - t0
+        if dt >= budget:
+            return flops, dt, rows
+
+
+def cpu_rate(kind, S, D, budget_s=12.0, workers=None):
+    """Aggregate CPU TFLOP/s of the reference kernels on this host: every core
+    runs causal row windows of one head -- a bounded sample of the same causal
+    workload (per-pair cost is what matters; heads are independent)."""
+    import multiprocessing as mpc
+    workers = workers or len(os.sched_getaffinity(0))
+    ctx = mpc.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_sample_worker, [(kind, S, D, budget_s, 100 + i)
+                                            for i in range(workers)])
+    wall = time.perf_counter() - t0
+    flops = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return {"flops": flops, "seconds": busy, "wall": wall, "workers": workers,
+            "rows": sum(r[2] for r in res), "tflops": flops / busy / 1e12}
+
+
+def reference_kind():
+    from oracle import ref_kernels
+    return "reference" if ref_kernels.load() is not None else "port"
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    S, H, D = a.seq, a.heads, a.head_dim
+    kind = reference_kind()
+    total = causal_flops(S, H, D)
+    rates = []
+    for i in range(a.warmup + a.steps):
+        r = cpu_rate(kind, S, D, budget_s=2.0)
+        if i >= a.warmup:
+            rates.append(r)
+    tflops = statistics.median(r["tflops"] for r in rates)
+    sec_per_step = total / (tflops * 1e12)
+    r0 = rates[0]
+    sample = (f"{r0['workers']} processes x 1 head, {r0['rows']} causal query rows (windows near the end "
+              f"of S={S} (keys 0..S), D={D}; {a.steps} timed samples; throughput extrapolated "
+              f"to the full workload ({total:.4e} flops)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform[-1,1) fp64)",
+        "config": workload_config(a, a.gpus),
+        "tokens_per_s": S / sec_per_step,
+        "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": r0["workers"],
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU side
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        loaded = [x for x in sm if mx and x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+def ncu_traffic():
+    """DRAM bytes per attention launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "attn_ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch_128k")
+    except Exception:
+        return None
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2412_20501_b200 import kernels, rng
+    from paper_2412_20501_b200.ring import TokenRingAttention
+
+    S, H, D = a.seq, a.heads, a.head_dim
+    runner = TokenRingAttention(S, H, D, causal=True, record_timeline=True)
+    q, k, v = rng.local_inputs(a.seed, runner.part, rank, H, D)
+    total_flops = causal_flops(S, H, D)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(fn, steps):
+        barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = s.elapsed_time(e) / steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    timelines = []
+
+    def step():
+        runner(q, k, v)
+        timelines.append(runner.timeline)
+
+    for _ in range(a.warmup):
+        step()
+    timelines.clear()
+    launches0 = kernels.LAUNCHES
+    with ClockSampler(local) as clk:
+        ms = timed(step, a.steps)
+    launches = (kernels.LAUNCHES - launches0) // a.steps * a.steps
+    torch.cuda.synchronize()
+
+    # exposed comm (stall of the compute stream on comm events) and the
+    # attention kernel's own device time, from the per-step CUDA events
+    stall, kern_ms, kern_flops, nlaunch = 0.0, 0.0, 0, 0
+    for tl in timelines:
+        for ev in tl:
+            stall += ev["start"].elapsed_time(ev["comm_ready"])
+            if "attn_start" in ev:
+                kern_ms += ev["attn_start"].elapsed_time(ev["attn_end"])
+                kern_flops += ev["attn_flops"]
+                nlaunch += 1
+    exposed = stall / max(1, len(timelines))
+    attn_avg_ms = kern_ms / max(1, nlaunch)
+    attn_flops_per_launch = kern_flops / max(1, nlaunch)
+    if world > 1:
+        t = torch.tensor([exposed, attn_avg_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        exposed, attn_avg_ms = (float(x) for x in t.tolist())
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+        qd, kd, vd = (torch.empty_like(t) for t in (q, k, v))
+        oh = torch.empty(runner.acc_out.shape, dtype=torch.bfloat16).pin_memory()
+        lh = torch.empty(runner.acc_lse.shape, dtype=torch.float32).pin_memory()
+        obf = torch.empty(runner.acc_out.shape, dtype=torch.bfloat16, device="cuda")
+
+        def e2e_step():
+            qd.copy_(qh, non_blocking=True)
+            kd.copy_(kh, non_blocking=True)
+            vd.copy_(vh, non_blocking=True)
+            res = runner(qd, kd, vd)
+            obf.copy_(res.out)
+            oh.copy_(obf, non_blocking=True)
+            lh.copy_(res.lse, non_blocking=True)
+
+        e2e_step()
+        e2e_ms = timed(e2e_step, max(1, min(a.steps, 5)))
+        h2d = 3 * q.numel() * 2 * world
+        d2h = (oh.numel() * 2 + lh.numel() * 4) * world
+        e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "api": "TokenRingAttention.__call__ -> tr_attention_segments / tr_merge_state "
+                      "(C ABI), pinned host buffers"}
+
+    if rank == 0:
+        peaks, peak_src = measured_peaks()
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        achieved = attn_flops_per_launch / (attn_avg_ms * 1e-3) / 1e12
+        line = {
+            "metric": METRIC, "value": total_flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": f"synthetic (SplitMix64 uniform[-1,1) -> bf16, seed {a.seed}, generated on "
+                    "device per rank shard)",
+            "config": workload_config(a, world),
+            "tokens_per_s": S / (ms * 1e-3),
+            "exposed_comm_ms_per_step": exposed,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic(),
+                         "kernel": "tr::attn_fwd_sm100_kernel<128>",
+                         "flops_per_launch": attn_flops_per_launch,
+                         "avg_launch_ms": attn_avg_ms,
+                         "peak_kind": f"bf16_tflops_sustained ({peak_src})",
+                         "frac_of_burst": achieved / peaks["bf16_tflops"],
+                         "frac_of_spec_2250": achieved / 2250.0},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if not a.no_cpu_baseline:
+            kind = reference_kind()
+            r = cpu_rate(kind, S, D, budget_s=12.0)
+            line["cpu_baseline"] = {
+                "value": r["tflops"], "unit": "TFLOP/s", "cores": r["workers"], "kind": kind,
+                "sample": f"{r['workers']} processes x 1 head, {r['rows']} causal query rows (windows near "
+                          f"the end of S={S} (keys 0..S), D={D}, {r['seconds']:.1f} s; "
+                          "throughput of the reference's CPU kernels on this host"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_ours(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

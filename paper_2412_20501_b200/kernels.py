@@ -26,6 +26,15 @@ MASK_CAUSAL = 2
 
 BACKEND = "cuda-sm100a"
 
+# Number of device kernels this process has launched through libtokenring
+# (bench.py reports the count inside its timed region as ``gpu_launches``).
+LAUNCHES = 0
+
+
+def _count(n):
+    global LAUNCHES
+    LAUNCHES += n
+
 
 def _stream(device=None):
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
@@ -70,6 +79,7 @@ def attention_block(q, k, v, mask_kind=MASK_NONE, q_offset=0, k_offset=0, out=No
     _lib.check(_lib.lib().tr_attention_block(
         _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), tq, tk, h, d, int(mask_kind),
         int(q_offset), int(k_offset), _stream(q.device)))
+    _count(1)
     return out, lse
 
 
@@ -92,6 +102,7 @@ def attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse):
     _lib.check(_lib.lib().tr_attention_segments(
         _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
         q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, _stream(q.device)))
+    _count(1)
     return out, lse
 
 
@@ -118,6 +129,7 @@ def merge_state_(acc_out, acc_lse, blk_out, blk_lse, final_out=None):
     _lib.check(_lib.lib().tr_merge_state(
         _ptr(acc_out), _ptr(acc_lse), _ptr(blk_out), dt, _ptr(blk_lse), t, h, d,
         acc_lse.stride(0), blk_lse.stride(0), fin, _stream(acc_out.device)))
+    _count(2)
     return acc_out, acc_lse
 
 
@@ -133,6 +145,7 @@ def partial_init_(acc_out, acc_lse):
     t, h, d = acc_out.shape
     _lib.check(_lib.lib().tr_partial_init(_ptr(acc_out), _ptr(acc_lse), t, h, d,
                                           _stream(acc_out.device)))
+    _count(1)
     return acc_out, acc_lse
 
 
@@ -142,4 +155,5 @@ def splitmix_bf16_(dst, seed, first, low=-1.0, high=1.0):
     _lib.check(_lib.lib().tr_splitmix_bf16(
         ctypes.c_uint64(int(seed) % (1 << 64)), int(first), dst.numel(), float(low), float(high),
         _ptr(dst), _stream(dst.device)))
+    _count(1)
     return dst

@@ -1,0 +1,289 @@
+"""Multi-GPU TokenRing: one process per GPU, torch.distributed for the
+plumbing (NCCL P2P over NVLink/NVSwitch), sm_100a kernels for the math.
+
+Per rank r and step i (schedule from ``engine.build_zigzag_token_ring`` /
+``build_token_ring``; semantics of ref engine.py:233-366, 468-638):
+
+    wait(comm[i-1])            Q_i has arrived; OUT returned at i-1 has arrived
+    merge returned OUT         lse-merge kernel into the float32 accumulator
+    issue comm[i]              send Q_i -> r+1, recv Q_{i+1} <- r-1,
+                               send OUT(step i-1) -> home, recv OUT <- sender
+    compute[i]                 ONE segmented attention launch (all q sub-chunks
+                               of the traveling set x both local kv sub-chunks)
+
+so the forward Q stream and the reverse OUT stream of step i run on the NCCL
+stream concurrently with compute[i] on the compute stream.  The final phase
+returns the last step's rows.  Double-buffered traveling-Q and output
+buffers make every hazard an ordering on the compute stream.
+
+Outputs stay sharded: rank r returns its home chunks in start order, exactly
+what ref ``engine.execute`` returns per rank, so ``global_reorder`` works.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import kernels
+from .core import Partial
+from .engine import MsgKind, build_token_ring, build_zigzag_token_ring, group_computes
+from .errors import ConfigError, DimensionError, ScheduleError
+
+
+class CudaOps:
+    """Device ops of the product path (libtokenring.so)."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+
+    def attention(self, q, k, v, q_segs, kv_segs, causal, out, lse):
+        kernels.attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse)
+
+    def merge_(self, acc_out, acc_lse, blk_out, blk_lse):
+        kernels.merge_state_(acc_out, acc_lse, blk_out, blk_lse)
+
+    def init_(self, acc_out, acc_lse):
+        kernels.partial_init_(acc_out, acc_lse)
+
+    def event(self):
+        return torch.cuda.Event(enable_timing=True)
+
+    def record(self, ev):
+        ev.record()
+
+
+@dataclass
+class RankStep:
+    step: int
+    q_layout: tuple          # chunk ids of the traveling Q buffer, in row order
+    q_ids: tuple             # q chunks computed this step
+    kv_ids: tuple            # local kv chunks used
+    accumulate: bool | None
+    send_q: tuple | None     # (dst, ids)
+    recv_q: tuple | None     # (src, ids)   -> layout of the next step's buffer
+    send_out: tuple | None   # (dst, ids)   rows from the previous step's output
+    recv_out: list           # [(src, ids)]  to merge after this step's comm
+
+
+def compile_rank(sched, rank: int) -> list:
+    """This rank's step program, derived from the schedule's plans."""
+    P = sched.ranks
+    plans = sched.all_plans()
+    layout = tuple(cid for cid in (c.id for c in sorted(
+        (c for c in sched.chunks if c.home == rank), key=lambda c: c.start)))
+    prog = []
+    for i, plan in enumerate(plans):
+        g = group_computes(sched, plan.computes[rank])
+        if g is None:
+            raise ScheduleError(f"step {i} rank {rank}: compute set not expressible as one launch")
+        q_ids, kv_ids, acc = g
+        send_q = send_out = recv_q = None
+        for m in plan.sends[rank]:
+            if m.kind is MsgKind.Q_BLOCK:
+                send_q = (m.dst, tuple(m.chunk_ids))
+            elif m.kind is MsgKind.OUT_LSE:
+                send_out = (m.dst, tuple(m.chunk_ids))
+            else:
+                raise ScheduleError("KV_BLOCK messages are not part of a token-ring program")
+        recv_out = []
+        for src in range(P):
+            for m in plan.sends[src]:
+                if m.dst != rank:
+                    continue
+                if m.kind is MsgKind.Q_BLOCK:
+                    recv_q = (src, tuple(m.chunk_ids))
+                elif m.kind is MsgKind.OUT_LSE:
+                    recv_out.append((src, tuple(m.chunk_ids)))
+        for a in q_ids:
+            if a not in layout:
+                raise ScheduleError(f"step {i} rank {rank}: q chunk {a} not resident")
+        prog.append(RankStep(i, layout, q_ids, kv_ids, acc, send_q, recv_q, send_out, recv_out))
+        if recv_q is not None:
+            layout = recv_q[1]
+    return prog
+
+
+def _rows(layout, ids, c):
+    """Contiguous row range of ``ids`` inside a buffer laid out as ``layout``."""
+    idx = [layout.index(a) for a in ids]
+    if idx != list(range(idx[0], idx[0] + len(idx))):
+        raise ScheduleError(f"chunks {ids} are not contiguous in buffer {layout}")
+    return idx[0] * c, (idx[0] + len(idx)) * c
+
+
+class TokenRingAttention:
+    """TokenRing forward on this process's rank of ``group``.
+
+    ``q_loc/k_loc/v_loc``: this rank's (S/P, H, D) bf16 shard -- its partition
+    ranges concatenated in start order (``partition.gather_local``).
+    Returns a float32 Partial over the same rows.
+    """
+
+    def __init__(self, seq_len, heads, head_dim, causal=True, group=None, ops=None,
+                 device=None, record_timeline=False):
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if causal:
+            self.sched = build_zigzag_token_ring(self.P, seq_len, heads, head_dim)
+        else:
+            self.sched = build_token_ring(self.P, seq_len, heads, head_dim)
+        self.causal = causal
+        self.S, self.H, self.D = seq_len, heads, head_dim
+        self.part = self.sched.partition
+        self.local_rows = self.part.owned_tokens(self.rank)
+        self.c = self.sched.chunks[0].tokens
+        self.prog = compile_rank(self.sched, self.rank)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.ops = ops if ops is not None else CudaOps(device)
+        self.device = self.ops.device
+        self.record_timeline = record_timeline
+        self.timeline = []
+        self._alloc()
+
+    def _alloc(self):
+        rows, H, D, dev = self.local_rows, self.H, self.D, self.device
+        bf = torch.bfloat16
+        self.qbuf = [torch.empty((rows, H, D), dtype=bf, device=dev) for _ in range(2)]
+        self.obuf = [torch.empty((rows, H, D), dtype=bf, device=dev) for _ in range(2)]
+        self.lbuf = [torch.empty((H, rows), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.lse_send = torch.empty((H, rows), dtype=torch.float32, device=dev)
+        self.out_recv = torch.empty((rows, H, D), dtype=bf, device=dev)
+        self.lse_recv = torch.empty((H, rows), dtype=torch.float32, device=dev)
+        self.acc_out = torch.empty((rows, H, D), dtype=torch.float32, device=dev)
+        self.acc_lse = torch.empty((H, rows), dtype=torch.float32, device=dev)
+
+    # -- transport -----------------------------------------------------------
+    def _comm(self, sends, recvs):
+        if self.P == 1 or not (sends or recvs):
+            return []
+        backend = dist.get_backend(self.group)
+        if backend == "nccl":
+            ops = [dist.P2POp(dist.isend, t, self._global(p), self.group) for p, t in sends]
+            ops += [dist.P2POp(dist.irecv, t, self._global(p), self.group) for p, t in recvs]
+            return dist.batch_isend_irecv(ops)
+        reqs = [dist.isend(t, self._global(p), self.group) for p, t in sends]
+        reqs += [dist.irecv(t, self._global(p), self.group) for p, t in recvs]
+        return reqs
+
+    def _global(self, r):
+        return r if self.group is None else dist.get_global_rank(self.group, r)
+
+    # -- one forward -----------------------------------------------------------
+    def __call__(self, q_loc, k_loc, v_loc) -> Partial:
+        shape = (self.local_rows, self.H, self.D)
+        for n, t in (("q", q_loc), ("k", k_loc), ("v", v_loc)):
+            if tuple(t.shape) != shape:
+                raise DimensionError(f"{n} shard must have shape {shape}, got {tuple(t.shape)}")
+        c, rank = self.c, self.rank
+        local_layout = self.prog[0].q_layout
+        self.ops.init_(self.acc_out, self.acc_lse)
+        pending, pending_out = [], None
+        self.timeline = []
+        for st in self.prog:
+            i = st.step
+            ev = {}
+            if self.record_timeline:
+                ev["start"] = self.ops.event()
+                self.ops.record(ev["start"])
+            for r in pending:
+                r.wait()
+            if self.record_timeline:
+                ev["comm_ready"] = self.ops.event()
+                self.ops.record(ev["comm_ready"])
+            if pending_out:
+                self._merge_returned(pending_out, local_layout)
+            sends, recvs = [], []
+            cur = self.qbuf[i % 2] if i > 0 else q_loc
+            if st.send_q is not None:
+                a, b = _rows(st.q_layout, st.send_q[1], c)
+                sends.append((st.send_q[0], cur[a:b]))
+            if st.recv_q is not None:
+                n = len(st.recv_q[1]) * c
+                recvs.append((st.recv_q[0], self.qbuf[(i + 1) % 2][:n]))
+            if st.send_out is not None:
+                prev_layout = self.prog[i - 1].q_layout
+                a, b = _rows(prev_layout, st.send_out[1], c)
+                ob, lb = self.obuf[(i - 1) % 2], self.lbuf[(i - 1) % 2]
+                ls = self.lse_send.view(-1)[: self.H * (b - a)].view(self.H, b - a)
+                ls.copy_(lb[:, a:b])
+                sends.append((st.send_out[0], ob[a:b]))
+                sends.append((st.send_out[0], ls))
+            pending_out = None
+            if st.recv_out:
+                if len(st.recv_out) != 1:
+                    raise ScheduleError(f"step {i} rank {rank}: more than one return per step")
+                src, ids = st.recv_out[0]
+                n = len(ids) * c
+                lr = self.lse_recv.view(-1)[: self.H * n].view(self.H, n)
+                recvs.append((src, self.out_recv[:n]))
+                recvs.append((src, lr))
+                pending_out = (ids, self.out_recv[:n], lr)
+            pending = self._comm(sends, recvs)
+            if st.q_ids:
+                q_segs = []
+                for a in st.q_ids:
+                    r0, _ = _rows(st.q_layout, (a,), c)
+                    q_segs.append((r0, c, self.sched.chunks[a].start))
+                kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
+                            self.sched.chunks[b].start) for b in st.kv_ids]
+                buf = i % 2
+                if self.record_timeline:
+                    ev["attn_start"] = self.ops.event()
+                    self.ops.record(ev["attn_start"])
+                self.ops.attention(cur, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                                   self.obuf[buf], self.lbuf[buf])
+                if self.record_timeline:
+                    ev["attn_end"] = self.ops.event()
+                    self.ops.record(ev["attn_end"])
+                    ev["attn_flops"] = self.step_flops(st)
+                if st.accumulate:
+                    for a in st.q_ids:
+                        r0, r1 = _rows(st.q_layout, (a,), c)
+                        l0 = self.part.local_offset(rank, self.sched.chunks[a].start)
+                        self.ops.merge_(self.acc_out[l0:l0 + c], self.acc_lse[:, l0:l0 + c],
+                                        self.obuf[buf][r0:r1], self.lbuf[buf][:, r0:r1])
+            if self.record_timeline:
+                ev["computed"] = self.ops.event()
+                self.ops.record(ev["computed"])
+                self.timeline.append(ev)
+        for r in pending:
+            r.wait()
+        if pending_out:
+            self._merge_returned(pending_out, local_layout)
+        return Partial(self.acc_out, self.acc_lse)
+
+    def step_flops(self, st) -> int:
+        """Algorithmic flops of one step's launch (ref engine.py:170-173)."""
+        from .engine import compute_flops
+        plan = self.sched.all_plans()[st.step]
+        ch = self.sched.chunks
+        return sum(compute_flops(cp.mask, ch[cp.q_chunk].tokens, ch[cp.kv_chunk].tokens,
+                                 self.H, self.D) for cp in plan.computes[self.rank])
+
+    def _merge_returned(self, pending_out, local_layout):
+        ids, out, lse = pending_out
+        c = self.c
+        for j, a in enumerate(ids):
+            if self.sched.chunks[a].home != self.rank:
+                raise ScheduleError(f"rank {self.rank}: returned chunk {a} homes elsewhere")
+            l0 = self.part.local_offset(self.rank, self.sched.chunks[a].start)
+            self.ops.merge_(self.acc_out[l0:l0 + c], self.acc_lse[:, l0:l0 + c],
+                            out[j * c:(j + 1) * c], lse[:, j * c:(j + 1) * c])
+
+
+def token_ring_attention(q_loc, k_loc, v_loc, seq_len, causal=True, group=None) -> Partial:
+    """Functional form: one TokenRing forward over ``group`` (all ranks call it)."""
+    h, d = q_loc.shape[1], q_loc.shape[2]
+    return TokenRingAttention(seq_len, h, d, causal, group, device=q_loc.device)(q_loc, k_loc, v_loc)
+
+
+def check_world(seq_len, causal, world):
+    """ConfigError early if the sequence does not split over ``world`` ranks."""
+    need = 2 * world if causal else world
+    if seq_len % need:
+        raise ConfigError(f"seq_len {seq_len} must be divisible by {need}")

@@ -1,0 +1,84 @@
+"""The C-ABI library: loads, exports every symbol include/tokenring.h
+declares, and its argument validation maps onto the reference's exception
+types.  CPU only (validation failures return before any device work)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "tokenring.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(tr_\w+)\s*\(", text, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2412_20501_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2412_20501_b200 import build
+        build.build()
+    return _lib
+
+
+def test_header_declares_expected_api():
+    fns = declared_functions()
+    assert fns == sorted(["tr_attention_block", "tr_attention_segments", "tr_merge_state",
+                          "tr_partial_init", "tr_splitmix_bf16", "tr_version",
+                          "tr_kernel_count", "tr_last_error"])
+
+
+def test_library_exports_every_declared_symbol(lib):
+    handle = lib.lib()
+    for name in declared_functions():
+        assert hasattr(handle, name), name
+    assert set(declared_functions()) == set(lib.EXPORTS)
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_version_and_probe(lib):
+    assert b"sm_100a" in lib.lib().tr_version()
+    assert lib.lib().tr_kernel_count() >= 5
+
+
+def test_validation_maps_to_reference_errors(lib):
+    from paper_2412_20501_b200.errors import ConfigError, DimensionError
+    L = lib.lib()
+    null = ctypes.c_void_p(0)
+    with pytest.raises(ConfigError):
+        lib.check(L.tr_attention_block(null, null, null, null, null, 4, 4, 1, 64, 7, 0, 0, null))
+    assert b"mask_kind" in L.tr_last_error()
+    with pytest.raises(DimensionError):
+        lib.check(L.tr_attention_block(null, null, null, null, null, 4, 4, 0, 64, 0, 0, 0, null))
+    with pytest.raises(DimensionError):
+        lib.check(L.tr_merge_state(null, null, null, 1, null, 8, 2, 64, 4, 8, null, null))
+    segs = (lib.Segment * 1)(lib.Segment(0, 10, 0))
+    with pytest.raises(DimensionError):   # segment runs past the 8-row buffer
+        lib.check(L.tr_attention_segments(null, null, null, null, null, 8, 8, 1, 64,
+                                          segs, 1, segs, 1, 1, null))
+    with pytest.raises(ConfigError):
+        lib.check(L.tr_attention_segments(null, null, null, null, null, 8, 8, 1, 64,
+                                          segs, 5, segs, 1, 1, null))
+    with pytest.raises(ConfigError):
+        lib.check(L.tr_splitmix_bf16(1, -1, 4, -1.0, 1.0, null, null))
+
+
+def test_sass_contains_tcgen05_and_tma(lib):
+    """The shipped library really carries tcgen05 MMA / TMEM / TMA code."""
+    sass = subprocess.run(["cuobjdump", "-sass", lib.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    if not sass:
+        pytest.skip("cuobjdump unavailable")
+    for mnem in ("UTCHMMA", "LDTM", "STTM", "UTMALDG"):
+        assert mnem in sass, mnem
+    assert "HMMA" not in re.sub(r"UTCHMMA", "", sass)

@@ -1,0 +1,77 @@
+"""The multi-process TokenRing runner (paper_2412_20501_b200.ring) at
+world_size 2 and 4 over gloo on CPU.  The device ops are replaced by the
+float64 oracle (test-only injection, tests/cpu_ops.py) so what is checked
+here is the host side: rank programs, buffer layouts, Q-forward and
+OUT-reverse P2P traffic and merge bookkeeping."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import kernels as ok
+from oracle import partition as opart
+from oracle import schedule as osch
+from oracle import splitmix
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, S, H, D, causal, seed, result_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_ops import OracleOps
+        from paper_2412_20501_b200.ring import TokenRingAttention
+        runner = TokenRingAttention(S, H, D, causal=causal, ops=OracleOps(), device="cpu")
+        q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(seed, S, H, D))
+        rng = runner.part.ranges(rank)
+        loc = [torch.as_tensor(opart.gather(x, rng), dtype=torch.float32).to(torch.bfloat16)
+               for x in (q, k, v)]
+        res = runner(*loc)
+        result_q.put((rank, res.out.double().numpy(), res.lse.double().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,S,H,D,causal", [(2, 64, 2, 8, True), (4, 128, 2, 8, True),
+                                               (2, 48, 2, 8, False), (3, 96, 1, 8, True)])
+def test_token_ring_gloo(world, S, H, D, causal):
+    ctx = mp.get_context("spawn")
+    q_ = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, S, H, D, causal, 11, q_))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, o, l = q_.get(timeout=120)
+        res[r] = (o, l)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(11, S, H, D))
+    sched = osch.zigzag_token_ring(world, S, H, D) if causal else osch.token_ring(world, S, H, D)
+    ref = osch.execute(sched, q, k, v)
+    for r in range(world):
+        # bf16 block outputs travel between ranks; accumulators stay float32
+        assert np.abs(res[r][0] - ref[r][0]).max() <= 2e-2
+        fin = np.isfinite(ref[r][1])
+        assert np.array_equal(np.isfinite(res[r][1]), fin)
+        assert np.abs(res[r][1][fin] - ref[r][1][fin]).max() <= 1e-3
+    g_out, g_lse = opart.reorder([res[r][0] for r in range(world)],
+                                 [res[r][1] for r in range(world)], osch.ranges_of(sched, S), S)
+    d_out, d_lse = ok.dense_attention(q, k, v, causal)
+    assert ok.max_relative_error(g_out, g_lse, d_out, d_lse) <= 2e-2
