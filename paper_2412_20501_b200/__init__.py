@@ -29,5 +29,6 @@ from .engine import (MessageTrace, MsgKind, Schedule, build_ring_attention,  # n
                      build_schedule, build_token_ring, build_zigzag_token_ring, comm_volume,
                      execute, trace_from_schedule)
 from .ring import TokenRingAttention, token_ring_attention  # noqa: F401,E402
+from . import core, engine, kernels, partition, ring, rng  # noqa: F401,E402
 
 __version__ = "0.1.0"
