@@ -44,12 +44,26 @@ struct AttnCfg {
   static constexpr uint32_t IDESC_QK = idesc_bf16(128, BN, false);
   static constexpr uint32_t IDESC_PV = idesc_bf16(128, D, true);
   static constexpr float RESCALE_LOG2 = 8.0f;
+  static constexpr int POLY_MOD = 4;   // 1 of every POLY_MOD exp2 pairs on the FMA pipe
 };
 
-struct KvCursor {
-  int64_t tiles[TR_MAX_SEGMENTS];
-  int total;
+// Per-CTA kv tile walk: the tile count of every kv segment lives in shared
+// memory (no dynamically indexed local arrays), and each role advances its
+// own (segment, tile) cursor.
+struct KvWalk {
+  int g;
+  int64_t t;
+  __device__ __forceinline__ void next(const int64_t* tiles) {
+    ++t;
+    while (g < TR_MAX_SEGMENTS - 1 && t >= tiles[g]) { t = 0; ++g; }
+  }
 };
+
+__device__ __forceinline__ KvWalk kv_begin(const int64_t* tiles) {
+  KvWalk w{0, 0};
+  while (w.g < TR_MAX_SEGMENTS - 1 && tiles[w.g] == 0) ++w.g;
+  return w;
+}
 
 __device__ __forceinline__ void q_tile_of(const AttnPlan& p, int64_t lin, int& seg, int64_t& row0) {
   seg = 0;
@@ -57,35 +71,6 @@ __device__ __forceinline__ void q_tile_of(const AttnPlan& p, int64_t lin, int& s
   int64_t local = lin - p.tile_prefix[seg];
   if (p.causal) local = (p.tile_prefix[seg + 1] - p.tile_prefix[seg]) - 1 - local;  // heavy first
   row0 = local * 256;
-}
-
-__device__ __forceinline__ KvCursor kv_tiles_for(const AttnPlan& p, int64_t qmax_pos) {
-  KvCursor c;
-  c.total = 0;
-  for (int g = 0; g < TR_MAX_SEGMENTS; ++g) {
-    int64_t n = 0;
-    if (g < p.nkv) {
-      n = (p.kv[g].rows + 127) / 128;
-      if (p.causal) {
-        if (qmax_pos < p.kv[g].pos0) n = 0;
-        else n = min(n, (qmax_pos - p.kv[g].pos0) / 128 + 1);
-      }
-    }
-    c.tiles[g] = n;
-    c.total += static_cast<int>(n);
-  }
-  return c;
-}
-
-// j-th kv tile of the cursor -> (local row of its first key, position, valid keys)
-__device__ __forceinline__ void kv_tile_at(const AttnPlan& p, const KvCursor& c, int j,
-                                           int64_t& row, int64_t& pos, int& valid) {
-  int g = 0;
-  int64_t t = j;
-  while (t >= c.tiles[g]) { t -= c.tiles[g]; ++g; }
-  row = p.kv[g].row0 + t * 128;
-  pos = p.kv[g].pos0 + t * 128;
-  valid = static_cast<int>(imin64(128, p.kv[g].rows - t * 128));
 }
 
 template <int D>
@@ -102,9 +87,10 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   uint64_t* kv_full = bars + 1;                 // [NS]
   uint64_t* kv_empty = bars + 1 + C::NS;        // [NS]
   uint64_t* s_full = bars + 1 + 2 * C::NS;      // [2]
-  uint64_t* p_full = bars + 3 + 2 * C::NS;      // [2]
-  uint64_t* o_done = bars + 5 + 2 * C::NS;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * C::NS);
+  uint64_t* p_full = bars + 3 + 2 * C::NS;      // [2 halves][2 key halves]
+  uint64_t* o_done = bars + 7 + 2 * C::NS;      // [2]
+  int64_t* kv_tiles = reinterpret_cast<int64_t*>(bars + 9 + 2 * C::NS);  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 2 * C::NS);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -115,23 +101,41 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   q_tile_of(p, lin, qseg, qrow0);
   const tr_segment Q = p.q[qseg];
   const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
-  const KvCursor kvc = kv_tiles_for(p, qmax_pos);
-  const int ntiles = kvc.total;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
-    for (int h = 0; h < 2; ++h) { mbar_init(&s_full[h], 1); mbar_init(&p_full[h], 128); mbar_init(&o_done[h], 1); }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&s_full[h], 1);
+      mbar_init(&p_full[2 * h], 128);
+      mbar_init(&p_full[2 * h + 1], 128);
+      mbar_init(&o_done[h], 1);
+    }
     fence_barrier_init();
     tma_prefetch_desc(&tmq); tma_prefetch_desc(&tmk); tma_prefetch_desc(&tmv);
+  }
+  if (warp == 2 && lane < TR_MAX_SEGMENTS) {
+    // kv tiles of every segment this q tile needs (causal: keys up to qmax_pos)
+    int64_t n = 0;
+    if (lane < p.nkv) {
+      n = (p.kv[lane].rows + 127) / 128;
+      if (p.causal)
+        n = (qmax_pos < p.kv[lane].pos0) ? 0 : imin64(n, (qmax_pos - p.kv[lane].pos0) / 128 + 1);
+    }
+    kv_tiles[lane] = n;
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int ntiles = static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]);
 
-  if (warp == 0) {
+  // Register rebalancing: each role's code sits inside the branch of its own
+  // setmaxnreg so ptxas compiles it against that budget.
+  if (warp < 4) {
+   setmaxnreg_dec<56>();
+   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0 && ntiles > 0) {
       const int32_t col0 = head * D;
@@ -140,11 +144,10 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         for (int b = 0; b < C::NB; ++b)
           tma_load_2d(sQ + (h * C::NB + b) * C::BOX, &tmq, q_full, col0 + 64 * b,
                       static_cast<int32_t>(Q.row0 + qrow0 + 128 * h), kEvictFirst);
+      KvWalk w = kv_begin(kv_tiles);
       int n = 0;
-      for (int j = 0; j < ntiles; ++j) {
-        int64_t krow, kpos;
-        int valid;
-        kv_tile_at(p, kvc, j, krow, kpos, valid);
+      for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
+        const int32_t krow = static_cast<int32_t>(p.kv[w.g].row0 + w.t * 128);
         for (int which = 0; which < 2; ++which, ++n) {
           const int s = n % C::NS;
           const uint32_t round = n / C::NS;
@@ -152,33 +155,49 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
           mbar_arrive_expect_tx(&kv_full[s], C::TILE);
           const CUtensorMap* tm = which ? &tmv : &tmk;
           for (int b = 0; b < C::NB; ++b)
-            tma_load_2d(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b,
-                        static_cast<int32_t>(krow), kEvictLast);
+            tma_load_2d(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b, krow,
+                        kEvictLast);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && ntiles > 0) {
-      const uint32_t tS[2] = {tmem + 0, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 384};
       const uint32_t q_addr = smem_u32(sQ);
       const uint32_t kv_addr = smem_u32(sKV);
       mbar_wait(q_full, 0);
       tc_fence_after();
+      // Descriptors differ only in the start-address field (bits 0..13, in
+      // 16-byte units), so each MMA adds an offset to one of two bases.
+      const uint64_t dK = sdesc_sw128(kv_addr, 16, 1024);       // Q and K: K-major
+      const uint64_t dQ = sdesc_sw128(q_addr, 16, 1024);
+      const uint64_t dV = sdesc_sw128(kv_addr, C::BOX, 1024);   // V: MN-major
       auto qk = [&](int h, int stage) {
+        const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
+        const uint64_t b0 = dK + static_cast<uint32_t>((stage * C::TILE) >> 4);
+        #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk / 4) * C::BOX + (kk % 4) * 32;
-          const uint64_t a = sdesc_sw128(q_addr + h * C::TILE + off, 16, 1024);
-          const uint64_t b = sdesc_sw128(kv_addr + stage * C::TILE + off, 16, 1024);
-          mma_ss(tS[h], a, b, C::IDESC_QK, kk > 0);
+          const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
+          mma_ss(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
         }
       };
-      auto pv = [&](int h, int stage, bool acc) {
-        for (int kk = 0; kk < C::BN / 16; ++kk) {
-          const uint64_t b = sdesc_sw128(kv_addr + stage * C::TILE + kk * 2048, C::BOX, 1024);
-          mma_ts(tO[h], tS[h] + kk * 8, b, C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+      // O_h += P_h[:, keys of half kh] . V[keys of half kh, :]
+      auto pv = [&](int h, int stage, int kh, bool acc) {
+        const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
+        #pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int kk = kh * 4 + k4;
+          mma_ts(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
+                 C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
         }
+      };
+      auto pv_both = [&](int h, int stage, uint32_t phase, bool acc) {
+        mbar_wait(&p_full[2 * h], phase);
+        tc_fence_after();
+        pv(h, stage, 0, acc);
+        mbar_wait(&p_full[2 * h + 1], phase);
+        tc_fence_after();
+        pv(h, stage, 1, true);
       };
       int prev_v_stage = 0;
       for (int j = 0; j < ntiles; ++j) {
@@ -189,28 +208,25 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         qk(0, sk);
         tc_commit(&s_full[0]);
         if (j > 0) {
-          mbar_wait(&p_full[1], (j - 1) & 1);
-          tc_fence_after();
-          pv(1, prev_v_stage, j - 1 > 0);
+          pv_both(1, prev_v_stage, (j - 1) & 1, j - 1 > 0);
           tc_commit(&kv_empty[prev_v_stage]);
         }
         qk(1, sk);
         tc_commit(&s_full[1]);
         tc_commit(&kv_empty[sk]);
         mbar_wait(&kv_full[sv], (nv / C::NS) & 1);
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        pv(0, sv, j > 0);
+        pv_both(0, sv, j & 1, j > 0);
         if (j == ntiles - 1) tc_commit(&o_done[0]);
         prev_v_stage = sv;
       }
-      mbar_wait(&p_full[1], (ntiles - 1) & 1);
-      tc_fence_after();
-      pv(1, prev_v_stage, ntiles - 1 > 0);
+      pv_both(1, prev_v_stage, (ntiles - 1) & 1, ntiles - 1 > 0);
       tc_commit(&kv_empty[prev_v_stage]);
       tc_commit(&o_done[1]);
     }
-  } else if (warp >= 4) {
+   }
+  } else {
+   setmaxnreg_inc<224>();
+   {
     // ------------------------------------------------------------ softmax + epilogue
     const int h = (warp - 4) / 4;         // which 128-row half
     const int quarter = warp % 4;         // TMEM lane quarter
@@ -223,38 +239,38 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     const int64_t half_min_pos = Q.pos0 + qrow0 + 128 * h;
     const float c = p.scale_log2;
     const float thresh = C::RESCALE_LOG2 / c;
+    const uint64_t c2 = f2pack(c, c);
     float m_used = -INFINITY;
-    float l = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
-      int64_t krow, kpos;
-      int valid;
-      kv_tile_at(p, kvc, j, krow, kpos, valid);
+    uint64_t lsum2[2] = {0ull, 0ull};     // packed partial row sums
+    KvWalk w = kv_begin(kv_tiles);
+    for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
+      const int64_t kpos = p.kv[w.g].pos0 + w.t * 128;
+      const int valid = static_cast<int>(imin64(128, p.kv[w.g].rows - w.t * 128));
       mbar_wait(&s_full[h], j & 1);
       tc_fence_after();
-      float s[128];
-      #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t u[32];
-        tmem_ld32(tS + cc * 32, u);
-        tc_wait_ld();
-        #pragma unroll
-        for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(u[i]);
-      }
+      uint32_t s[128];
+      tmem_ld32_at<0>(tS + 0, s);
+      tmem_ld32_at<32>(tS + 32, s);
+      tmem_ld32_at<64>(tS + 64, s);
+      tmem_ld32_at<96>(tS + 96, s);
+      tc_wait_ld();
+      // masking is decided per 128-row half (uniform across the warpgroup)
       const bool need_mask = valid < 128 || (p.causal && kpos + 127 > half_min_pos);
       if (need_mask) {
         int64_t lim = valid;
         if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
         const int limit = static_cast<int>(imax64(lim, 0));
         #pragma unroll
-        for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : -INFINITY;
+        for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;  // -inf
       }
-      float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+      float mx = __uint_as_float(s[0]);
+      float mxb = __uint_as_float(s[1]);
       #pragma unroll
-      for (int i = 4; i < 128; i += 4) {
-        mx0 = fmaxf(mx0, s[i]); mx1 = fmaxf(mx1, s[i + 1]);
-        mx2 = fmaxf(mx2, s[i + 2]); mx3 = fmaxf(mx3, s[i + 3]);
+      for (int i = 2; i < 128; i += 4) {
+        mx = fmaxf(mx, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
+        mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
       }
-      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+      mx = fmaxf(mx, mxb);
       const bool grow = mx > m_used + thresh;
       const bool scale_o = grow && m_used != -INFINITY;
       // tcgen05.ld/st are warp-collective: decide per warp, scale per row.
@@ -262,37 +278,62 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         // O holds only completed P.V products (this tile's S commit implies
         // every earlier MMA finished); rescale it before publishing P_j.
         const float f = scale_o ? ex2_approx((m_used - mx) * c) : 1.f;
-        l *= f;
+        const uint64_t f2 = f2pack(f, f);
+        lsum2[0] = fmul2(lsum2[0], f2);
+        lsum2[1] = fmul2(lsum2[1], f2);
         #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
           uint32_t u[32];
           tmem_ld32(tO + cc * 32, u);
           tc_wait_ld();
           #pragma unroll
-          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * f);
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t v = fmul2(f2pack(__uint_as_float(u[i]), __uint_as_float(u[i + 1])), f2);
+            u[i] = static_cast<uint32_t>(v);
+            u[i + 1] = static_cast<uint32_t>(v >> 32);
+          }
           tmem_st32(tO + cc * 32, u);
         }
       }
       if (grow) m_used = mx;
       const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
-      float l0 = 0.f, l1 = 0.f;
+      const uint64_t nmc2 = f2pack(-mc, -mc);
+      // P = exp2(s*c - m*c), bf16, written over S's first 64 columns in two
+      // key halves so the P.V MMA can start on the first half early.
       #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
+      for (int kh = 0; kh < 2; ++kh) {
         uint32_t pk[32];
         #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float a = ex2_approx(fmaf(s[cc * 64 + 2 * i], c, -mc));
-          const float b = ex2_approx(fmaf(s[cc * 64 + 2 * i + 1], c, -mc));
-          l0 += a;
-          l1 += b;
-          pk[i] = pack_bf16x2(a, b);
+          const int e = kh * 64 + 2 * i;
+          const uint64_t x2 = ffma2(f2pack(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), c2, nmc2);
+          uint64_t p2;
+          if ((i % C::POLY_MOD) == C::POLY_MOD - 1 && !need_mask) {
+            float a, b;
+            f2unpack(x2, a, b);
+            p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f)));
+          } else {
+            float a, b;
+            f2unpack(x2, a, b);
+            p2 = f2pack(ex2_approx(a), ex2_approx(b));
+          }
+          lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
+          float pa, pb;
+          f2unpack(p2, pa, pb);
+          pk[i] = pack_bf16x2(pa, pb);
         }
-        tmem_st32(tS + cc * 32, pk);
+        tmem_st32(tS + kh * 32, pk);
+        tc_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * h + kh]);
       }
-      l += l0 + l1;
-      tc_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_full[h]);
+    }
+    float l;
+    {
+      float a0, a1, b0, b1;
+      f2unpack(lsum2[0], a0, a1);
+      f2unpack(lsum2[1], b0, b1);
+      l = (a0 + a1) + (b0 + b1);
     }
     // ---------------------------------------------------------- epilogue
     const bool row_ok = row_in_seg < Q.rows;
@@ -325,6 +366,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     }
     if (row_ok)
       p.lse[head * p.lse_stride + grow] = (l > 0.f) ? (logf(l) + m_used * p.scale) : -INFINITY;
+   }
   }
   tc_fence_before();
   __syncthreads();

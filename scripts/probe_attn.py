@@ -28,6 +28,7 @@ def bench(fn, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--case", type=int, default=-1, help="run only this case index")
     a = ap.parse_args()
     cases = [
         ("causal S=32768 H=32 D=128", 32768, 32768, 32, 128, 2),
@@ -36,6 +37,8 @@ def main():
         ("causal S=131072 H=32 D=128", 131072, 131072, 32, 128, 2),
         ("full 4096x4096 H=8 D=64", 4096, 4096, 8, 64, 0),
     ]
+    if a.case >= 0:
+        cases = [cases[a.case]]
     for name, tq, tk, h, d, mask in cases:
         q = torch.randn(tq, h, d, device="cuda").to(torch.bfloat16) * 0.5
         k = torch.randn(tk, h, d, device="cuda").to(torch.bfloat16) * 0.5
