@@ -73,6 +73,37 @@ __device__ __forceinline__ void q_tile_of(const AttnPlan& p, int64_t lin, int& s
   row0 = local * 256;
 }
 
+// exp2 of one S row (already in registers) -> bf16 P in TMEM, row sums in
+// packed accumulators; arrives on pbar[kh] after each 64-key half.
+template <int POLY_MOD, bool kPoly>
+__device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, uint64_t c2,
+                                       uint64_t nmc2, uint64_t (&lsum2)[2], uint64_t* pbar) {
+  #pragma unroll
+  for (int kh = 0; kh < 2; ++kh) {
+    uint32_t pk[32];
+    #pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int e = kh * 64 + 2 * i;
+      const uint64_t x2 = ffma2(f2pack(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), c2, nmc2);
+      float a, b;
+      f2unpack(x2, a, b);
+      uint64_t p2;
+      if (kPoly && (i % POLY_MOD) == POLY_MOD - 1)
+        p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f)));
+      else
+        p2 = f2pack(ex2_approx(a), ex2_approx(b));
+      lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
+      float pa, pb;
+      f2unpack(p2, pa, pb);
+      pk[i] = pack_bf16x2(pa, pb);
+    }
+    tmem_st32(tS + kh * 32, pk);
+    tc_wait_st();
+    tc_fence_before();
+    mbar_arrive(&pbar[kh]);
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(384, 1)
 attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
@@ -135,94 +166,98 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   // setmaxnreg so ptxas compiles it against that budget.
   if (warp < 4) {
    setmaxnreg_dec<56>();
-   if (warp == 0) {
+   if (warp == 0 && ntiles > 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0 && ntiles > 0) {
-      const int32_t col0 = head * D;
-      mbar_arrive_expect_tx(q_full, 2 * C::TILE);
-      for (int h = 0; h < 2; ++h)
+    // The whole warp walks the loop (warp-uniform state in uniform
+    // registers); elect.sync inside each asm picks the issuing lane.
+    const int32_t col0 = head * D;
+    mbar_arrive_expect_tx_elect(q_full, 2 * C::TILE);
+    for (int h = 0; h < 2; ++h)
+      for (int b = 0; b < C::NB; ++b)
+        tma_load_2d_elect(sQ + (h * C::NB + b) * C::BOX, &tmq, q_full, col0 + 64 * b,
+                          static_cast<int32_t>(Q.row0 + qrow0 + 128 * h), kEvictFirst);
+    KvWalk w = kv_begin(kv_tiles);
+    int s = 0;
+    uint32_t round = 0;
+    for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
+      const int32_t krow = static_cast<int32_t>(p.kv[w.g].row0 + w.t * 128);
+      #pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        mbar_wait(&kv_empty[s], (round & 1) ^ 1);
+        mbar_arrive_expect_tx_elect(&kv_full[s], C::TILE);
+        const CUtensorMap* tm = which ? &tmv : &tmk;
+        #pragma unroll
         for (int b = 0; b < C::NB; ++b)
-          tma_load_2d(sQ + (h * C::NB + b) * C::BOX, &tmq, q_full, col0 + 64 * b,
-                      static_cast<int32_t>(Q.row0 + qrow0 + 128 * h), kEvictFirst);
-      KvWalk w = kv_begin(kv_tiles);
-      int n = 0;
-      for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
-        const int32_t krow = static_cast<int32_t>(p.kv[w.g].row0 + w.t * 128);
-        for (int which = 0; which < 2; ++which, ++n) {
-          const int s = n % C::NS;
-          const uint32_t round = n / C::NS;
-          mbar_wait(&kv_empty[s], (round & 1) ^ 1);
-          mbar_arrive_expect_tx(&kv_full[s], C::TILE);
-          const CUtensorMap* tm = which ? &tmv : &tmk;
-          for (int b = 0; b < C::NB; ++b)
-            tma_load_2d(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b, krow,
-                        kEvictLast);
-        }
+          tma_load_2d_elect(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b, krow,
+                            kEvictLast);
+        if (++s == C::NS) { s = 0; ++round; }
       }
     }
-  } else if (warp == 1) {
+   } else if (warp == 1 && ntiles > 0) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && ntiles > 0) {
-      const uint32_t q_addr = smem_u32(sQ);
-      const uint32_t kv_addr = smem_u32(sKV);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      // Descriptors differ only in the start-address field (bits 0..13, in
-      // 16-byte units), so each MMA adds an offset to one of two bases.
-      const uint64_t dK = sdesc_sw128(kv_addr, 16, 1024);       // Q and K: K-major
-      const uint64_t dQ = sdesc_sw128(q_addr, 16, 1024);
-      const uint64_t dV = sdesc_sw128(kv_addr, C::BOX, 1024);   // V: MN-major
-      auto qk = [&](int h, int stage) {
-        const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
-        const uint64_t b0 = dK + static_cast<uint32_t>((stage * C::TILE) >> 4);
-        #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
-          mma_ss(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
-        }
-      };
-      // O_h += P_h[:, keys of half kh] . V[keys of half kh, :]
-      auto pv = [&](int h, int stage, int kh, bool acc) {
-        const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
-        #pragma unroll
-        for (int k4 = 0; k4 < 4; ++k4) {
-          const int kk = kh * 4 + k4;
-          mma_ts(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
-                 C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
-        }
-      };
-      auto pv_both = [&](int h, int stage, uint32_t phase, bool acc) {
-        mbar_wait(&p_full[2 * h], phase);
-        tc_fence_after();
-        pv(h, stage, 0, acc);
-        mbar_wait(&p_full[2 * h + 1], phase);
-        tc_fence_after();
-        pv(h, stage, 1, true);
-      };
-      int prev_v_stage = 0;
-      for (int j = 0; j < ntiles; ++j) {
-        const int nk = 2 * j, nv = 2 * j + 1;
-        const int sk = nk % C::NS, sv = nv % C::NS;
-        mbar_wait(&kv_full[sk], (nk / C::NS) & 1);
-        tc_fence_after();
-        qk(0, sk);
-        tc_commit(&s_full[0]);
-        if (j > 0) {
-          pv_both(1, prev_v_stage, (j - 1) & 1, j - 1 > 0);
-          tc_commit(&kv_empty[prev_v_stage]);
-        }
-        qk(1, sk);
-        tc_commit(&s_full[1]);
-        tc_commit(&kv_empty[sk]);
-        mbar_wait(&kv_full[sv], (nv / C::NS) & 1);
-        pv_both(0, sv, j & 1, j > 0);
-        if (j == ntiles - 1) tc_commit(&o_done[0]);
-        prev_v_stage = sv;
+    const uint32_t q_addr = smem_u32(sQ);
+    const uint32_t kv_addr = smem_u32(sKV);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    // Descriptors differ only in the start-address field (bits 0..13, in
+    // 16-byte units), so each MMA adds an offset to one of three bases.
+    const uint64_t dK = sdesc_sw128(kv_addr, 16, 1024);       // Q and K: K-major
+    const uint64_t dQ = sdesc_sw128(q_addr, 16, 1024);
+    const uint64_t dV = sdesc_sw128(kv_addr, C::BOX, 1024);   // V: MN-major
+    auto qk = [&](int h, int stage) {
+      const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
+      const uint64_t b0 = dK + static_cast<uint32_t>((stage * C::TILE) >> 4);
+      #pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
+        mma_ss_elect(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
       }
-      pv_both(1, prev_v_stage, (ntiles - 1) & 1, ntiles - 1 > 0);
-      tc_commit(&kv_empty[prev_v_stage]);
-      tc_commit(&o_done[1]);
+    };
+    // O_h += P_h[:, keys of half kh] . V[keys of half kh, :]
+    auto pv = [&](int h, int stage, int kh, bool acc) {
+      const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
+      #pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int kk = kh * 4 + k4;
+        mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
+                     C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+      }
+    };
+    auto pv_both = [&](int h, int stage, uint32_t phase, bool acc) {
+      mbar_wait(&p_full[2 * h], phase);
+      tc_fence_after();
+      pv(h, stage, 0, acc);
+      mbar_wait(&p_full[2 * h + 1], phase);
+      tc_fence_after();
+      pv(h, stage, 1, true);
+    };
+    int prev_v_stage = 0;
+    int sk = 0;
+    uint32_t rk = 0;     // ring position / round of K_j (V_j follows it)
+    for (int j = 0; j < ntiles; ++j) {
+      const int sv = (sk + 1 == C::NS) ? 0 : sk + 1;
+      const uint32_t rv = (sk + 1 == C::NS) ? rk + 1 : rk;
+      mbar_wait(&kv_full[sk], rk & 1);
+      tc_fence_after();
+      qk(0, sk);
+      tc_commit_elect(&s_full[0]);
+      if (j > 0) {
+        pv_both(1, prev_v_stage, (j - 1) & 1, j - 1 > 0);
+        tc_commit_elect(&kv_empty[prev_v_stage]);
+      }
+      qk(1, sk);
+      tc_commit_elect(&s_full[1]);
+      tc_commit_elect(&kv_empty[sk]);
+      mbar_wait(&kv_full[sv], rv & 1);
+      pv_both(0, sv, j & 1, j > 0);
+      if (j == ntiles - 1) tc_commit_elect(&o_done[0]);
+      prev_v_stage = sv;
+      sk = (sv + 1 == C::NS) ? 0 : sv + 1;
+      rk = (sv + 1 == C::NS) ? rv + 1 : rv;
     }
+    pv_both(1, prev_v_stage, (ntiles - 1) & 1, ntiles - 1 > 0);
+    tc_commit_elect(&kv_empty[prev_v_stage]);
+    tc_commit_elect(&o_done[1]);
    }
   } else {
    setmaxnreg_inc<224>();
@@ -299,34 +334,13 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
       const uint64_t nmc2 = f2pack(-mc, -mc);
       // P = exp2(s*c - m*c), bf16, written over S's first 64 columns in two
-      // key halves so the P.V MMA can start on the first half early.
-      #pragma unroll
-      for (int kh = 0; kh < 2; ++kh) {
-        uint32_t pk[32];
-        #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int e = kh * 64 + 2 * i;
-          const uint64_t x2 = ffma2(f2pack(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), c2, nmc2);
-          uint64_t p2;
-          if ((i % C::POLY_MOD) == C::POLY_MOD - 1 && !need_mask) {
-            float a, b;
-            f2unpack(x2, a, b);
-            p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f)));
-          } else {
-            float a, b;
-            f2unpack(x2, a, b);
-            p2 = f2pack(ex2_approx(a), ex2_approx(b));
-          }
-          lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
-          float pa, pb;
-          f2unpack(p2, pa, pb);
-          pk[i] = pack_bf16x2(pa, pb);
-        }
-        tmem_st32(tS + kh * 32, pk);
-        tc_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_full[2 * h + kh]);
-      }
+      // key halves so the P.V MMA can start on the first half early.  Masked
+      // tiles keep every exp2 on MUFU (exact 0 for -inf); full tiles move one
+      // pair in POLY_MOD to the FMA pipe.
+      if (need_mask)
+        emit_p<C::POLY_MOD, false>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
+      else
+        emit_p<C::POLY_MOD, true>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
     }
     float l;
     {

@@ -120,6 +120,47 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// ---- warp-uniform "elected" forms: the whole warp executes the instruction
+// stream (so every operand stays warp-uniform and lives in uniform
+// registers) and elect.sync predicates the single issuing lane inside the asm.
+__device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_elect(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_elect(void* smem_dst, const void* tmap, uint64_t* bar,
+                                                  int32_t c0, int32_t c1, uint64_t cache_hint) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;\n}\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
+      : "memory");
+}
+
 // Shared-memory matrix descriptor, 128-byte swizzle, sm_100 version bits.
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes,
                                                 uint32_t sbo_bytes) {
@@ -242,9 +283,16 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   uint64_t p = ffma2(f, 0x3D61FA703D61FA70ull /*0.0551704764*/, 0x3E786E5A3E786E5Aull /*0.2426084578*/);
   p = ffma2(p, f, 0x3F31798D3F31798Dull /*0.6932609677*/);
   p = ffma2(p, f, 0x3F7FFB4C3F7FFB4Cull /*0.9999282360*/);
-  const uint32_t tl = static_cast<uint32_t>(t), th = static_cast<uint32_t>(t >> 32);
-  const uint32_t pl = static_cast<uint32_t>(p), ph = static_cast<uint32_t>(p >> 32);
-  return (static_cast<uint64_t>(ph + (th << 23)) << 32) | static_cast<uint64_t>(pl + (tl << 23));
+  // result bits = p_bits + (t_bits << 23): one IMAD per element (the magic's
+  // own exponent/mantissa bits shift out of the 32-bit word)
+  uint64_t r;
+  asm("{\n.reg .b32 tl, th, pl, ph;\n"
+      "mov.b64 {tl, th}, %1;\nmov.b64 {pl, ph}, %2;\n"
+      "mad.lo.u32 pl, tl, 8388608, pl;\nmad.lo.u32 ph, th, 8388608, ph;\n"
+      "mov.b64 %0, {pl, ph};\n}\n"
+      : "=l"(r)
+      : "l"(t), "l"(p));
+  return r;
 }
 
 // pack (lo, hi) -> bf16x2 with lo in the low 16 bits (RNE)
