@@ -13,7 +13,7 @@ import threading
 from .errors import ConfigError, DimensionError, InputError, RingsimError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtokenring.so")
+LIB_PATH = os.environ.get("TOKENRING_LIB") or os.path.join(HERE, "libtokenring.so")
 
 TR_OK = 0
 TR_ERR_DIMENSION = -1

@@ -37,15 +37,19 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile every .cu and link libtokenring.so (or ``out`` -- tuning
+    variants built with extra -D ``defines``)."""
+    lib = out or LIB
+    if not force and not defines and not _stale():
         return LIB
     objs = []
-    tmp = os.path.join(HERE, "_build")
+    tmp = os.path.join(HERE, "_build", "_".join(d.replace("=", "") for d in defines) or "main")
     os.makedirs(tmp, exist_ok=True)
     nvcc = nvcc_path()
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+              "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr",
+              *[f"-D{d}" for d in defines]]
     if verbose:
         common += ["-Xptxas", "-v"]
     procs = []
@@ -60,20 +64,22 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}:\n{out.decode()}")
         if verbose:
             print(out.decode())
-    link = [nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
+    link = [nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--out", default=None)
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, defines=tuple(a.defines), out=a.out))
 
 
 if __name__ == "__main__":

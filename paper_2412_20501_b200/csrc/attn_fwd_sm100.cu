@@ -44,12 +44,30 @@ struct AttnCfg {
   static constexpr uint32_t IDESC_QK = idesc_bf16(128, BN, false);
   static constexpr uint32_t IDESC_PV = idesc_bf16(128, D, true);
   static constexpr float RESCALE_LOG2 = 8.0f;
-  static constexpr int POLY_MOD = 4;   // 1 of every POLY_MOD exp2 pairs on the FMA pipe
+#ifndef TR_POLY_MOD
+#define TR_POLY_MOD 4
+#endif
+  static constexpr int POLY_MOD = TR_POLY_MOD;   // 1 of every POLY_MOD exp2 pairs on the FMA pipe
 };
 
 // Per-CTA kv tile walk: the tile count of every kv segment lives in shared
 // memory (no dynamically indexed local arrays), and each role advances its
 // own (segment, tile) cursor.
+#ifdef TR_TRACE
+// Debug-only timeline of CTA 0 (clock64 per role and kv tile); read back with
+// tr_debug_trace().  Not compiled into the product library.
+__device__ unsigned long long g_trace[12 * 64 * 8];
+#define TR_TRACE_AT(slot, jj)                                                        \
+  do {                                                                               \
+    if (blockIdx.x == 0 && lane == 0 && (jj) < 64)                                   \
+      g_trace[(warp * 64 + (jj)) * 8 + (slot)] = clock64();                          \
+  } while (0)
+#else
+#define TR_TRACE_AT(slot, jj) \
+  do {                        \
+  } while (0)
+#endif
+
 struct KvWalk {
   int g;
   int64_t t;
@@ -159,8 +177,11 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int ntiles = static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]);
+  // shared-memory loads are per-thread values to the compiler; broadcasting
+  // them makes them provably warp-uniform (uniform-datapath MMA issue)
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const int ntiles = __shfl_sync(
+      0xffffffffu, static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]), 0);
 
   // Register rebalancing: each role's code sits inside the branch of its own
   // setmaxnreg so ptxas compiles it against that budget.
@@ -239,7 +260,9 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       const uint32_t rv = (sk + 1 == C::NS) ? rk + 1 : rk;
       mbar_wait(&kv_full[sk], rk & 1);
       tc_fence_after();
+      TR_TRACE_AT(0, j);
       qk(0, sk);
+      TR_TRACE_AT(1, j);
       tc_commit_elect(&s_full[0]);
       if (j > 0) {
         pv_both(1, prev_v_stage, (j - 1) & 1, j - 1 > 0);
@@ -281,8 +304,17 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
       const int64_t kpos = p.kv[w.g].pos0 + w.t * 128;
       const int valid = static_cast<int>(imin64(128, p.kv[w.g].rows - w.t * 128));
+      TR_TRACE_AT(0, j);
       mbar_wait(&s_full[h], j & 1);
+      TR_TRACE_AT(1, j);
       tc_fence_after();
+#ifdef TR_EXP_NOSOFTMAX
+      // experiment: measure the MMA/TMA pipeline alone (results are garbage)
+      tc_fence_before();
+      mbar_arrive(&p_full[2 * h]);
+      mbar_arrive(&p_full[2 * h + 1]);
+      continue;
+#endif
       uint32_t s[128];
       tmem_ld32_at<0>(tS + 0, s);
       tmem_ld32_at<32>(tS + 32, s);
@@ -306,6 +338,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
       }
       mx = fmaxf(mx, mxb);
+      TR_TRACE_AT(2, j);
       const bool grow = mx > m_used + thresh;
       const bool scale_o = grow && m_used != -INFINITY;
       // tcgen05.ld/st are warp-collective: decide per warp, scale per row.
@@ -341,6 +374,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         emit_p<C::POLY_MOD, false>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
       else
         emit_p<C::POLY_MOD, true>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
+      TR_TRACE_AT(3, j);
     }
     float l;
     {
@@ -389,6 +423,13 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     tmem_dealloc(tmem, 512);
   }
 }
+
+#ifdef TR_TRACE
+extern "C" int tr_debug_trace(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace)) ==
+                 cudaSuccess ? 0 : -4;
+}
+#endif
 
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,

@@ -40,6 +40,8 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#if defined(TR_WAIT_HINT)
+  // explicit suspend-time hint: compiles to TRYWAIT + NANOSLEEP.SYNCS
   asm volatile(
       "{\n.reg .pred P1;\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, 1000000;\n"
@@ -47,6 +49,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#else
+  // no hint: the hardware's own bounded TRYWAIT (wakes on the phase flip)
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+#endif
   return ok != 0;
 }
 // Wait for the phase with the given parity.  A pipeline bug must not wedge the
