@@ -414,7 +414,7 @@ def group_computes(sched: Schedule, computes) -> tuple | None:
 
 
 # ----------------------------------------------------------------- executor
-def execute(sched: Schedule, q, k, v, causal: bool | None = None):
+def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list | None = None):
     """Run a schedule with all simulated ranks on the current GPU.
 
     Same contract as ``ringsim.engine.execute`` (ref engine.py:468-638):
@@ -422,6 +422,9 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None):
     MessageTrace) and raises ScheduleError naming step and rank when a
     compute touches a chunk that was never delivered or a return is
     unexpected.  Partials are float32 (out) / float32 (lse) on the device.
+    If ``timeline`` is a list, (step, rank, start_event, end_event) CUDA
+    event pairs bracketing every rank's attention launch are appended to it
+    (the measured counterpart of the reference's netsim compute lane).
     """
     if causal is not None and causal != sched.causal:
         raise ConfigError(f"schedule was built causal={sched.causal}, got causal={causal}")
@@ -513,8 +516,15 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None):
             qs, ks, accumulate = g
             q_segs = [(ch[a].start, ch[a].tokens, ch[a].start) for a in qs]
             kv_segs = [(ch[b].start, ch[b].tokens, ch[b].start) for b in ks]
+            if timeline is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
             kernels.attention_segments(q, k, v, q_segs, kv_segs, sched.causal,
                                        stage_out[buf], stage_lse[buf])
+            if timeline is not None:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record()
+                timeline.append((step, r, ev0, ev1))
             if accumulate:
                 for a in sorted(qs):
                     if ch[a].home != r:

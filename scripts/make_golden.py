@@ -238,7 +238,22 @@ def exec_cases():
     return arrs, meta
 
 
+def cli_volumes():
+    """ringsim.cli volume output for the configs shipped in configs/."""
+    import io
+    from ringsim import cli
+    cfg_dir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "configs")
+    res = {}
+    for name in sorted(os.listdir(cfg_dir)):
+        buf = io.StringIO()
+        cli.cmd_volume(cli.load_config(os.path.join(cfg_dir, name)), out=buf)
+        res[name] = buf.getvalue()
+    return res
+
+
 def main():
+    with open(os.path.join(OUT, "cli_volume.json"), "w") as f:
+        json.dump(cli_volumes(), f, indent=1)
     with open(os.path.join(OUT, "rng_kats.json"), "w") as f:
         json.dump(rng_kats(), f, indent=1)
     arrs, meta = kernel_cases()

@@ -1,0 +1,103 @@
+"""The ringsim-compatible CLI: config schema, exit codes and the volume
+report match the reference (CPU); verify / profile / compare on the GPU."""
+
+import io
+import json
+import os
+
+import pytest
+
+from conftest import ROOT, load_json
+from paper_2412_20501_b200 import cli
+from paper_2412_20501_b200.errors import ConfigError
+
+CFG = os.path.join(ROOT, "configs")
+
+
+def write(tmp_path, data):
+    p = tmp_path / "cfg.json"
+    p.write_text(json.dumps(data))
+    return str(p)
+
+
+BASE = {"problem": {"seq_len": 64, "heads": 2, "head_dim": 16, "causal": True, "seed": 1},
+        "parallel": {"ranks": 4, "nodes": 1}, "schedule": {"kind": "zigzag-token-ring"}}
+
+
+def test_volume_matches_reference_output():
+    gold = load_json("cli_volume.json")
+    assert set(gold) == set(os.listdir(CFG))
+    for name, text in gold.items():
+        buf = io.StringIO()
+        assert cli.cmd_volume(cli.load_config(os.path.join(CFG, name)), out=buf) == 0
+        assert buf.getvalue() == text, name
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda d: d.update(extra={}), "unknown config section"),
+    (lambda d: d["problem"].update(dtype="bf16"), "unknown key"),
+    (lambda d: d["problem"].update(causal=False), "requires causal=true"),
+    (lambda d: d["problem"].update(seq_len=60), "2P must divide seq_len"),
+    (lambda d: d["schedule"].update(kind="hybrid"), "not part of the B200 path"),
+    (lambda d: d["schedule"].update(kind="bogus"), "unknown schedule kind"),
+    (lambda d: d.update(topology={"kind": "torus"}), "unknown topology kind"),
+    (lambda d: d.update(timing={"efficiency": 1.5}), "efficiency"),
+    (lambda d: d["parallel"].update(ranks=0), "ranks must be a positive integer"),
+])
+def test_config_validation(mutate, msg):
+    data = json.loads(json.dumps(BASE))
+    mutate(data)
+    with pytest.raises(ConfigError, match=msg):
+        cli.RunConfig.from_dict(data)
+
+
+def test_token_ring_rejects_causal():
+    data = json.loads(json.dumps(BASE))
+    data["schedule"]["kind"] = "token-ring"
+    with pytest.raises(ConfigError, match="requires causal=false"):
+        cli.RunConfig.from_dict(data)
+
+
+def test_exit_codes(tmp_path, capsys):
+    bad = write(tmp_path, {"problem": {}})
+    assert cli.main(["volume", "--config", bad]) == 2
+    assert cli.main(["volume", "--config", str(tmp_path / "missing.json")]) == 3
+    assert cli.main(["volume", "--config", write(tmp_path, BASE)]) == 0
+    assert cli.main(["bogus"]) == 2
+
+
+def test_parse_sweep():
+    assert cli.parse_sweep("seq_len=4096..32768") == ("seq_len", [4096, 8192, 16384, 32768])
+    with pytest.raises(ConfigError):
+        cli.parse_sweep("heads=1..4")
+
+
+def test_switch_model_charges_ports():
+    cfg = cli.RunConfig.from_dict(json.loads(json.dumps(BASE)))
+    sched = cli.build_schedule(cfg)
+    send, recv = cli.modelled_comm(cfg, sched)
+    assert len(send) == sched.n_steps and all(len(r) == 4 for r in send)
+    assert max(send[0]) > 0 and max(recv[-1]) > 0
+
+
+@pytest.mark.gpu
+def test_verify_profile_compare_on_gpu(tmp_path, capsys):
+    assert cli.main(["verify", "--config", os.path.join(CFG, "example_verify.json")]) == 0
+    assert "status=PASS" in capsys.readouterr().out
+    assert cli.main(["verify", "--config", write(tmp_path, BASE)]) == 0
+    t, s = tmp_path / "t.json", tmp_path / "s.csv"
+    assert cli.main(["profile", "--config", write(tmp_path, BASE), "--trace", str(t),
+                     "--summary", str(s)]) == 0
+    events = json.loads(t.read_text())
+    assert {e["tid"] for e in events} <= {"compute", "send", "recv"}
+    assert all(e["ph"] == "X" and isinstance(e["ts"], int) for e in events)
+    lines = s.read_text().splitlines()
+    assert lines[0] == cli.SUMMARY_HEADER and lines[-1].split(",")[5] == "total"
+    capsys.readouterr()
+    data = json.loads(json.dumps(BASE))
+    data["problem"]["causal"] = False
+    data["schedule"]["kind"] = "token-ring"
+    assert cli.main(["compare", "--config", write(tmp_path, data), "--schedules",
+                     "ring,token-ring", "--sweep", "seq_len=64..128"]) == 0
+    rows = capsys.readouterr().out.splitlines()
+    assert rows[0] == cli.COMPARE_HEADER and len(rows) == 5
