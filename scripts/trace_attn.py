@@ -32,3 +32,7 @@ for w in (4, 8):
     print(f"softmax warp {w}: period {np.median(np.diff(s[8:60, 1])):.0f}  S ready->max "
           f"{np.median(s[8:60, 2] - s[8:60, 1]):.0f}  max->P done {np.median(s[8:60, 3] - s[8:60, 2]):.0f}"
           f"  P done->next S ready {np.median(s[9:61, 1] - s[8:60, 3]):.0f}")
+print("softmax phases (median cycles): S ready->max, max->half0 computed, ->half0 published, ->half1 computed, ->half1 published")
+for w in (4, 5, 6, 7, 8):
+    s = t[w][8:60]
+    print(w, [int(np.median(s[:, b] - s[:, a])) for a, b in ((1, 2), (2, 4), (4, 5), (5, 6), (6, 7))])
