@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N>1 exchange: NCCL P2P (default) or copy-engine CUDA IPC")
     return ap.parse_args()
 
 
@@ -315,7 +317,8 @@ def run_ours(a):
     from paper_2412_20501_b200.ring import TokenRingAttention
 
     S, H, D = a.seq, a.heads, a.head_dim
-    runner = TokenRingAttention(S, H, D, causal=True, record_timeline=True)
+    runner = TokenRingAttention(S, H, D, causal=True, record_timeline=True,
+                                transport=a.transport)
     q, k, v = rng.local_inputs(a.seed, runner.part, rank, H, D)
     total_flops = causal_flops(S, H, D)
 

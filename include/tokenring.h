@@ -97,6 +97,16 @@ int tr_partial_init(float* acc_out, float* acc_lse, int64_t tokens, int32_t head
 int tr_splitmix_bf16(uint64_t seed, int64_t first, int64_t count, double low, double high,
                      void* dst, void* stream);
 
+/* Copy-engine transport support (CUDA IPC / NVLink peer memory).  A sender
+ * cudaMemcpyAsync's a block into the peer's mapped receive buffer and then
+ * raises the peer's 64-bit sequence flag with a system-scope release store;
+ * the receiver's stream spins (one thread, acquire loads) until its flag
+ * reaches the expected value.  Replaces the in-process message delivery of
+ * engine.execute (pkg/src/ringsim/engine.py:515-518, 595-619). */
+int tr_flag_set(uint64_t* flag, uint64_t value, void* stream);
+int tr_flag_wait(const uint64_t* flag, uint64_t value, void* stream);
+int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
+
 /* Version / capability probes (no GPU work). */
 const char* tr_version(void);
 int32_t tr_kernel_count(void);

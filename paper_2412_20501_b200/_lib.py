@@ -27,7 +27,8 @@ TR_DTYPE_BF16 = 1
 
 # every symbol include/tokenring.h declares
 EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_merge_state", "tr_partial_init",
-           "tr_splitmix_bf16", "tr_version", "tr_kernel_count", "tr_last_error")
+           "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_copy_async", "tr_version",
+           "tr_kernel_count", "tr_last_error")
 
 
 class CudaError(RingsimError, RuntimeError):
@@ -57,8 +58,12 @@ def _declare(lib):
     lib.tr_partial_init.argtypes = [vp, vp, i64, i32, i32, vp]
     lib.tr_splitmix_bf16.argtypes = [ctypes.c_uint64, i64, i64, ctypes.c_double,
                                      ctypes.c_double, vp, vp]
+    lib.tr_flag_set.argtypes = [vp, ctypes.c_uint64, vp]
+    lib.tr_flag_wait.argtypes = [vp, ctypes.c_uint64, vp]
+    lib.tr_copy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
     for name in ("tr_attention_block", "tr_attention_segments", "tr_merge_state",
-                 "tr_partial_init", "tr_splitmix_bf16"):
+                 "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
+                 "tr_copy_async"):
         getattr(lib, name).restype = ctypes.c_int
     lib.tr_version.restype = ctypes.c_char_p
     lib.tr_version.argtypes = []

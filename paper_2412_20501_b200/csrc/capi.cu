@@ -29,6 +29,8 @@ int launch_partial_init(float* acc_out, float* acc_lse, int64_t T, int H, int D,
 int launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 int launch_splitmix(uint64_t seed, int64_t first, int64_t count, double low, double high,
                     void* dst, cudaStream_t s);
+int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s);
+int launch_flag_wait(const unsigned long long* flag, unsigned long long value, cudaStream_t s);
 
 static int check_segments(const tr_segment* segs, int n, int64_t total, const char* what) {
   if (n < 0 || n > TR_MAX_SEGMENTS)
@@ -131,8 +133,28 @@ int tr_splitmix_bf16(uint64_t seed, int64_t first, int64_t count, double low, do
   return launch_splitmix(seed, first, count, low, high, dst, static_cast<cudaStream_t>(stream));
 }
 
+int tr_flag_set(uint64_t* flag, uint64_t value, void* stream) {
+  if (!flag) return fail(TR_ERR_INPUT, "null flag");
+  return launch_flag_set(reinterpret_cast<unsigned long long*>(flag), value,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int tr_flag_wait(const uint64_t* flag, uint64_t value, void* stream) {
+  if (!flag) return fail(TR_ERR_INPUT, "null flag");
+  return launch_flag_wait(reinterpret_cast<const unsigned long long*>(flag), value,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return TR_OK;
+  if (!dst || !src) return fail(TR_ERR_INPUT, "null pointer");
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
+                                     static_cast<cudaStream_t>(stream)),
+                     "tr_copy_async");
+}
+
 const char* tr_version(void) { return "tokenring-b200 0.1 (sm_100a)"; }
-int32_t tr_kernel_count(void) { return 7; }
+int32_t tr_kernel_count(void) { return 9; }
 const char* tr_last_error(void) { return g_last_error.c_str(); }
 
 }  // extern "C"

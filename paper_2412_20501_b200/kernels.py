@@ -157,3 +157,30 @@ def splitmix_bf16_(dst, seed, first, low=-1.0, high=1.0):
         _ptr(dst), _stream(dst.device)))
     _count(1)
     return dst
+
+
+def flag_set_(flag, value, stream=None):
+    """Raise a (possibly peer-mapped) int64 sequence flag after all prior work
+    on ``stream`` (system-scope release store)."""
+    s = stream or torch.cuda.current_stream(flag.device)
+    _lib.check(_lib.lib().tr_flag_set(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
+    _count(1)
+
+
+def flag_wait_(flag, value, stream=None):
+    """Make ``stream`` wait until ``flag >= value`` (one-thread acquire spin)."""
+    s = stream or torch.cuda.current_stream(flag.device)
+    _lib.check(_lib.lib().tr_flag_wait(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
+    _count(1)
+
+
+def copy_(dst, src, stream=None):
+    """Copy-engine transfer (cudaMemcpyAsync, UVA) between contiguous tensors,
+    local or peer-mapped; no SMs are used."""
+    if dst.numel() * dst.element_size() != src.numel() * src.element_size():
+        raise DimensionError("copy_ size mismatch")
+    if not (dst.is_contiguous() and src.is_contiguous()):
+        raise DimensionError("copy_ needs contiguous tensors")
+    s = stream or torch.cuda.current_stream(src.device)
+    _lib.check(_lib.lib().tr_copy_async(_ptr(dst), _ptr(src), dst.numel() * dst.element_size(),
+                                        ctypes.c_void_p(s.cuda_stream)))

@@ -123,7 +123,7 @@ class TokenRingAttention:
     """
 
     def __init__(self, seq_len, heads, head_dim, causal=True, group=None, ops=None,
-                 device=None, record_timeline=False):
+                 device=None, record_timeline=False, transport="nccl"):
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -143,7 +143,12 @@ class TokenRingAttention:
         self.device = self.ops.device
         self.record_timeline = record_timeline
         self.timeline = []
+        if transport not in ("nccl", "ipc"):
+            raise ConfigError(f"transport must be 'nccl' or 'ipc', got {transport!r}")
+        self.transport = transport if self.P > 1 else "nccl"
         self._alloc()
+        if self.transport == "ipc":
+            self._ipc_setup()
 
     def _alloc(self):
         rows, H, D, dev = self.local_rows, self.H, self.D, self.device
@@ -174,7 +179,126 @@ class TokenRingAttention:
         return r if self.group is None else dist.get_global_rank(self.group, r)
 
     # -- one forward -----------------------------------------------------------
+    # -- copy-engine transport (CUDA IPC / NVLink peer memory) ----------------
+    # Every rank exposes its receive buffers and a flag block to all peers
+    # (torch's CUDA IPC handles, exchanged once over the process group).  A
+    # send is a cudaMemcpyAsync straight into the peer's buffer on this rank's
+    # copy stream -- copy engines, no SMs taken from the attention kernel --
+    # followed by a release store to the peer's sequence flag.
+    #   flags[0] q_ready : highest step whose Q for me has landed
+    #   flags[1] q_free  : highest step whose traveling-Q slot I am done with
+    #   flags[2] o_ready : highest step whose returned OUT for me has landed
+    #   flags[3] o_free  : highest step whose returned OUT I have merged
+    def _ipc_setup(self):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.flags = torch.zeros(8, dtype=torch.int64, device=self.device)
+        mine = [reduce_tensor(t) for t in (self.qbuf[0], self.qbuf[1], self.out_recv,
+                                           self.lse_recv, self.flags)]
+        everyone = [None] * self.P
+        dist.all_gather_object(everyone, mine, group=self.group)
+        self.peer = {}
+        for r in range(self.P):
+            if r == self.rank:
+                continue
+            fn_args = everyone[r]
+            self.peer[r] = [fn(*args) for fn, args in fn_args]
+        self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.calls = 0
+
+    def _forward_ipc(self, q_loc, k_loc, v_loc) -> Partial:
+        c, rank, P = self.c, self.rank, self.P
+        base = self.calls * (P + 4) + 8
+        self.calls += 1
+        cur = torch.cuda.current_stream(self.device)
+        cs = self.copy_stream
+        # initial conditions of this call, visible to every peer before anyone sends
+        self.flags[:4] = torch.tensor([base - 1, base, base - 1, base + 1], dtype=torch.int64)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        self.ops.init_(self.acc_out, self.acc_lse)
+        local_layout = self.prog[0].q_layout
+        ev_comp, ev_out_sent = {}, {}
+        for st in self.prog:
+            i = st.step
+            if i >= 1 and (st.q_ids or st.send_q is not None):
+                kernels.flag_wait_(self.flags[0:1], base + i, cur)       # Q_i has landed
+            if i >= 1 and self.prog[i - 1].recv_out:
+                # OUT sent to me at step i-1 has landed: merge it, free the buffer
+                kernels.flag_wait_(self.flags[2:3], base + i - 1, cur)
+                src, ids = self.prog[i - 1].recv_out[0]
+                n = len(ids) * c
+                self._merge_returned((ids, self.out_recv[:n],
+                                      self.lse_recv.view(-1)[: self.H * n].view(self.H, n)),
+                                     local_layout)
+                kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
+            cur_q = self.qbuf[i % 2] if i > 0 else q_loc
+            ev_q = torch.cuda.Event()
+            ev_q.record(cur)
+            if st.send_q is not None:
+                dst, ids = st.send_q
+                a, b = _rows(st.q_layout, ids, c)
+                cs.wait_event(ev_q)
+                kernels.flag_wait_(self.peer[dst][4][1:2], base + i - 1, cs)   # peer slot free
+                kernels.copy_(self.peer[dst][(i + 1) % 2][: b - a], cur_q[a:b], cs)
+                kernels.flag_set_(self.peer[dst][4][0:1], base + i + 1, cs)
+            if st.send_out is not None:
+                dst, ids = st.send_out
+                a, b = _rows(self.prog[i - 1].q_layout, ids, c)
+                cs.wait_event(ev_comp[i - 1])
+                kernels.flag_wait_(self.peer[dst][4][3:4], base + i - 1, cs)   # home buffer free
+                ob, lb = self.obuf[(i - 1) % 2], self.lbuf[(i - 1) % 2]
+                ls = self.lse_send.view(-1)[: self.H * (b - a)].view(self.H, b - a)
+                with torch.cuda.stream(cs):
+                    ls.copy_(lb[:, a:b])
+                kernels.copy_(self.peer[dst][2][: b - a], ob[a:b], cs)
+                kernels.copy_(self.peer[dst][3].view(-1)[: self.H * (b - a)], ls, cs)
+                kernels.flag_set_(self.peer[dst][4][2:3], base + i, cs)
+                ev_out_sent[i] = torch.cuda.Event()
+                ev_out_sent[i].record(cs)
+            if st.q_ids:
+                if (i - 1) in ev_out_sent:                 # obuf[i%2] was read by that send
+                    cur.wait_event(ev_out_sent[i - 1])
+                q_segs = [(_rows(st.q_layout, (a,), c)[0], c, self.sched.chunks[a].start)
+                          for a in st.q_ids]
+                kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
+                            self.sched.chunks[b].start) for b in st.kv_ids]
+                buf = i % 2
+                self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                                   self.obuf[buf], self.lbuf[buf])
+                if st.accumulate:
+                    for a in st.q_ids:
+                        r0, r1 = _rows(st.q_layout, (a,), c)
+                        l0 = self.part.local_offset(rank, self.sched.chunks[a].start)
+                        self.ops.merge_(self.acc_out[l0:l0 + c], self.acc_lse[:, l0:l0 + c],
+                                        self.obuf[buf][r0:r1], self.lbuf[buf][:, r0:r1])
+            ev_comp[i] = torch.cuda.Event()
+            ev_comp[i].record(cur)
+            if i < P:
+                # my traveling-Q slot i%2 is free once both this step's compute
+                # and my own forward copy of it are done
+                cs.wait_event(ev_comp[i])
+                kernels.flag_set_(self.flags[1:2], base + i, cs)
+        last = self.prog[-1]
+        if last.recv_out:
+            kernels.flag_wait_(self.flags[2:3], base + last.step, cur)
+            src, ids = last.recv_out[0]
+            n = len(ids) * c
+            self._merge_returned((ids, self.out_recv[:n],
+                                  self.lse_recv.view(-1)[: self.H * n].view(self.H, n)),
+                                 local_layout)
+        cur.wait_stream(cs)
+        return Partial(self.acc_out, self.acc_lse)
+
     def __call__(self, q_loc, k_loc, v_loc) -> Partial:
+        if self.transport == "ipc":
+            shape = (self.local_rows, self.H, self.D)
+            for n, t in (("q", q_loc), ("k", k_loc), ("v", v_loc)):
+                if tuple(t.shape) != shape:
+                    raise DimensionError(f"{n} shard must have shape {shape}, got {tuple(t.shape)}")
+            return self._forward_ipc(q_loc, k_loc, v_loc)
+        return self._forward_p2p(q_loc, k_loc, v_loc)
+
+    def _forward_p2p(self, q_loc, k_loc, v_loc) -> Partial:
         shape = (self.local_rows, self.H, self.D)
         for n, t in (("q", q_loc), ("k", k_loc), ("v", v_loc)):
             if tuple(t.shape) != shape:
