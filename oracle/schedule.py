@@ -79,30 +79,57 @@ def ring(p, seq_len, h, d, causal=False):           # ref engine.py:203-230
             "steps": steps, "final": None}
 
 
-def token_ring(p, seq_len, h, d):                   # ref engine.py:233-295 (nodes=1)
+def node_ring(kind, nodes, g, seq_len, h, d):      # ref engine.py:233-290
+    """Token ring inside each node of g ranks, KV hand-off across nodes."""
+    p = nodes * g
     part.contiguous(seq_len, p)
     if p == 1:
-        return _trivial("token-ring", seq_len, False)
+        return _trivial(kind, seq_len, False)
     n = seq_len // p
     chunks = [[r, r * n, (r + 1) * n, r] for r in range(p)]
-    steps = []
-    for s in range(p):
-        plan = _plan(p)
-        for r in range(p):
-            resident = (r - s) % p
-            plan[r]["computes"].append([resident, r, "none", 0, 0, s == 0])
-            if s < p - 1:
-                plan[r]["sends"].append([(r + 1) % p, "q_block", [resident], _q_el(n, h, d)])
-            if s >= 2:
-                prev = (r - s + 1) % p
-                plan[r]["sends"].append([prev, "out_lse", [prev], _out_el(n, h, d)])
-        steps.append(plan)
-    final = _plan(p)
-    for r in range(p):
-        prev = (r - p + 1) % p
-        final[r]["sends"].append([prev, "out_lse", [prev], _out_el(n, h, d)])
-    return _wire_merges({"kind": "token-ring", "ranks": p, "causal": False,
-                         "chunks": chunks, "steps": steps, "final": final})
+    steps, final = [], None
+    for ph in range(nodes):
+        s0 = ph % g
+        for s in range(g):
+            plan = _plan(p)
+            for m in range(nodes):
+                for loc in range(g):
+                    r = m * g + loc
+                    resident = m * g + (loc + ph - s) % g
+                    kv = ((m - ph) % nodes) * g + loc
+                    plan[r]["computes"].append([resident, kv, "none", 0, 0, s == s0])
+                    if s < g - 1:
+                        plan[r]["sends"].append([m * g + (loc + 1) % g, "q_block", [resident],
+                                                 _q_el(n, h, d)])
+                    if s >= 1 and (s - 1) != s0:
+                        prev = m * g + (loc + ph - (s - 1)) % g
+                        plan[r]["sends"].append([prev, "out_lse", [prev], _out_el(n, h, d)])
+            steps.append(plan)
+        ret = _plan(p)
+        for m in range(nodes):
+            for loc in range(g):
+                r = m * g + loc
+                if (g - 1) != s0:
+                    prev = m * g + (loc + ph - (g - 1)) % g
+                    ret[r]["sends"].append([prev, "out_lse", [prev], _out_el(n, h, d)])
+                if ph < nodes - 1:
+                    kv = ((m - ph) % nodes) * g + loc
+                    ret[r]["sends"].append([((m + 1) % nodes) * g + loc, "kv_block", [kv],
+                                            _kv_el(n, h, d)])
+        if ph < nodes - 1:
+            steps.append(ret)
+        else:
+            final = ret
+    return _wire_merges({"kind": kind, "ranks": p, "causal": False, "chunks": chunks,
+                         "steps": steps, "final": final})
+
+
+def token_ring(p, seq_len, h, d):                   # ref engine.py:293-295
+    return node_ring("token-ring", 1, p, seq_len, h, d)
+
+
+def hybrid(nodes, g, seq_len, h, d):                # ref engine.py:298-303
+    return node_ring("hybrid", nodes, g, seq_len, h, d)
 
 
 def zigzag_token_ring(p, seq_len, h, d):            # ref engine.py:306-366
@@ -152,6 +179,19 @@ def zigzag_token_ring(p, seq_len, h, d):            # ref engine.py:306-366
             final = plan
     return _wire_merges({"kind": "zigzag-token-ring", "ranks": p, "causal": True,
                          "chunks": chunks, "steps": steps, "final": final})
+
+
+def by_name(kind, p, seq_len, h, d, causal=False, nodes=1):
+    """Builder by the reference CLI's schedule names (ref cli.py:167-180)."""
+    if kind == "ring":
+        return ring(p, seq_len, h, d, causal)
+    if kind == "token-ring":
+        return token_ring(p, seq_len, h, d)
+    if kind == "hybrid":
+        return hybrid(nodes, p // nodes, seq_len, h, d)
+    if kind == "zigzag-token-ring":
+        return zigzag_token_ring(p, seq_len, h, d)
+    raise ValueError(kind)
 
 
 def ranges_of(sched, seq_len):

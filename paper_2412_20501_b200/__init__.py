@@ -8,7 +8,8 @@ A drop-in for the attention path of the reference ``ringsim`` package
 * partition:  Partition, split_contiguous, split_zigzag, causal_work_count,
               gather_local, global_reorder
 * engine:     MsgKind, Schedule, build_ring_attention, build_token_ring,
-              build_zigzag_token_ring, execute, trace_from_schedule, comm_volume
+              build_zigzag_token_ring (route="ring"|"direct"), build_hybrid,
+              execute, trace_from_schedule, comm_volume
 * ring:       TokenRingAttention / token_ring_attention (one process per GPU)
 * errors:     RingsimError, DimensionError, InputError, ConfigError,
               ScheduleError, TopologyError
@@ -26,7 +27,8 @@ from .kernels import BACKEND as KERNEL_BACKEND  # noqa: F401,E402
 from .core import (MaskKind, MaskSpec, Partial, block_attention,  # noqa: F401,E402
                    dense_attention, max_relative_error, merge_partial)
 from .engine import (MessageTrace, MsgKind, Schedule, build_ring_attention,  # noqa: F401,E402
-                     build_schedule, build_token_ring, build_zigzag_token_ring, comm_volume,
+                     build_hybrid, build_schedule, build_token_ring, build_zigzag_token_ring,
+                     comm_volume,
                      execute, trace_from_schedule)
 from .ring import TokenRingAttention, token_ring_attention  # noqa: F401,E402
 from . import core, engine, kernels, partition, ring, rng  # noqa: F401,E402

@@ -191,33 +191,70 @@ def build_ring_attention(ranks, seq_len, heads, head_dim, causal=False) -> Sched
     return Schedule("ring", ranks, heads, head_dim, causal, part, chunks, steps, None)
 
 
+def _node_ring(kind, nodes, per_node, seq_len, heads, head_dim) -> Schedule:
+    """TokenRing inside each node of ``per_node`` ranks, KV rotation across
+    ``nodes`` nodes (ref engine.py:233-290; nodes=1 is the plain TokenRing).
+
+    Phase p (one per node hop) has ``per_node`` steps.  Rank r = m*G + l holds
+    kv chunk ((m-p) mod M)*G + l during phase p; the q chunk resident at step
+    s is m*G + (l+p-s) mod G, so the rank meets its own q chunk (and
+    accumulates locally) at s0 = p mod G.  Every other step's rows go back to
+    the q chunk's home one step later.  Between phases a step with no
+    computes returns the last rows and hands kv chunks to the next node."""
+    M, G = nodes, per_node
+    P = M * G
+    part = split_contiguous(seq_len, P)
+    if P == 1:
+        return _trivial(kind, part, heads, head_dim, False)
+    n = seq_len // P
+    chunks = tuple(Chunk(r, r * n, (r + 1) * n, r) for r in range(P))
+    qe, ke = q_elements(n, heads, head_dim), kv_elements(n, heads, head_dim)
+    oe = out_lse_elements(n, heads, head_dim)
+    steps, final = [], None
+    for p in range(M):
+        s0 = p % G
+        for s in range(G):
+            plan = StepPlan.empty(P)
+            for r in range(P):
+                m, l = divmod(r, G)
+                resident = m * G + (l + p - s) % G
+                plan.computes[r].append(ComputePlan(resident, ((m - p) % M) * G + l,
+                                                    MaskSpec.none(), s == s0))
+                if s < G - 1:
+                    plan.sends[r].append(MsgPlan(r, m * G + (l + 1) % G, MsgKind.Q_BLOCK,
+                                                 (resident,), qe))
+                if s >= 1 and s - 1 != s0:
+                    prev = m * G + (l + p - s + 1) % G
+                    plan.sends[r].append(MsgPlan(r, prev, MsgKind.OUT_LSE, (prev,), oe))
+            steps.append(plan)
+        hand = StepPlan.empty(P)
+        for r in range(P):
+            m, l = divmod(r, G)
+            if G - 1 != s0:
+                prev = m * G + (l + p - G + 1) % G
+                hand.sends[r].append(MsgPlan(r, prev, MsgKind.OUT_LSE, (prev,), oe))
+            if p < M - 1:
+                hand.sends[r].append(MsgPlan(r, ((m + 1) % M) * G + l, MsgKind.KV_BLOCK,
+                                             (((m - p) % M) * G + l,), ke))
+        if p < M - 1:
+            steps.append(hand)
+        else:
+            final = hand
+    return _wire_merges(Schedule(kind, P, heads, head_dim, False, part, chunks, steps, final))
+
+
 def build_token_ring(ranks, seq_len, heads, head_dim) -> Schedule:
-    """Non-causal TokenRing (ref engine.py:233-295 with one node): q chunk
-    (r-s) mod P visits rank r at step s; results return to the chunk's home."""
-    part = split_contiguous(seq_len, ranks)
-    if ranks == 1:
-        return _trivial("token-ring", part, heads, head_dim, False)
-    n = seq_len // ranks
-    chunks = tuple(Chunk(r, r * n, (r + 1) * n, r) for r in range(ranks))
-    qe, oe = q_elements(n, heads, head_dim), out_lse_elements(n, heads, head_dim)
-    steps = []
-    for s in range(ranks):
-        plan = StepPlan.empty(ranks)
-        for r in range(ranks):
-            resident = (r - s) % ranks
-            plan.computes[r].append(ComputePlan(resident, r, MaskSpec.none(), s == 0))
-            if s < ranks - 1:
-                plan.sends[r].append(MsgPlan(r, (r + 1) % ranks, MsgKind.Q_BLOCK, (resident,), qe))
-            if s >= 2:
-                home = (r - s + 1) % ranks
-                plan.sends[r].append(MsgPlan(r, home, MsgKind.OUT_LSE, (home,), oe))
-        steps.append(plan)
-    final = StepPlan.empty(ranks)
-    for r in range(ranks):
-        home = (r + 1) % ranks
-        final.sends[r].append(MsgPlan(r, home, MsgKind.OUT_LSE, (home,), oe))
-    return _wire_merges(Schedule("token-ring", ranks, heads, head_dim, False, part, chunks,
-                                 steps, final))
+    """Non-causal TokenRing (ref engine.py:293-295): q chunk (r-s) mod P
+    visits rank r at step s; results return to the chunk's home."""
+    return _node_ring("token-ring", 1, ranks, seq_len, heads, head_dim)
+
+
+def build_hybrid(nodes, ranks_per_node, seq_len, heads, head_dim) -> Schedule:
+    """TokenRing inside each node, KV rotation across nodes, non-causal
+    (ref engine.py:298-303)."""
+    if nodes < 1 or ranks_per_node < 1:
+        raise ConfigError("nodes and ranks_per_node must be >= 1")
+    return _node_ring("hybrid", nodes, ranks_per_node, seq_len, heads, head_dim)
 
 
 def zigzag_alive(ranks: int, origin: int, step: int) -> tuple:
@@ -230,11 +267,36 @@ def zigzag_alive(ranks: int, origin: int, step: int) -> tuple:
     return (origin, high) if (origin >= 1 or step == 0) else (high,)
 
 
-def build_zigzag_token_ring(ranks, seq_len, heads, head_dim) -> Schedule:
-    """Causal TokenRing over the zigzag partition (ref engine.py:306-366)."""
+def _direct_carries_low(P: int, origin: int, sender: int) -> bool:
+    """Direct routing: does the ring hop sender -> sender+1 carry origin's low chunk?
+
+    The low chunk ``origin`` is computed only at its origin (step 0) and at
+    hosts 0..origin-1 (after the wrap), so on a full mesh it goes straight
+    from its origin to host 0 and rides the ring only for hops 0 -> 1 -> ...
+    -> origin-1, i.e. from senders 0..origin-2."""
+    return origin >= 1 and 0 <= sender <= origin - 2
+
+
+def build_zigzag_token_ring(ranks, seq_len, heads, head_dim, route: str = "ring") -> Schedule:
+    """Causal TokenRing over the zigzag partition (ref engine.py:306-366).
+
+    ``route="ring"`` is the reference schedule, message for message.
+    ``route="direct"`` (NOT a reference schedule) keeps
+    every compute of the reference at the same rank and step but stops
+    carrying a low sub-chunk through the hosts that do not compute it
+    (ref engine.py:346-353 forwards it through hosts origin+1..P-1): origin
+    o keeps its low chunk o until step P-o-1 and then sends it directly to
+    host 0, which needs it at step P-o, over the NVSwitch full mesh.  It
+    arrives in the same step and the same buffer position as on the ring,
+    so no extra buffers exist; the Q bytes drop by (P-1)(P-2)/2 chunk-hops
+    out of (P-1)(2P-1)."""
+    if route not in ("ring", "direct"):
+        raise ConfigError(f"route must be 'ring' or 'direct', got {route!r}")
+    direct = route == "direct"
+    kind = "zigzag-token-ring-direct" if direct else "zigzag-token-ring"
     part = split_zigzag(seq_len, ranks)
     if ranks == 1:
-        return _trivial("zigzag-token-ring", part, heads, head_dim, True)
+        return _trivial(kind, part, heads, head_dim, True)
     P = ranks
     c = seq_len // (2 * P)
     chunks = tuple(Chunk(a, a * c, (a + 1) * c, min(a, 2 * P - 1 - a)) for a in range(2 * P))
@@ -262,6 +324,14 @@ def build_zigzag_token_ring(ranks, seq_len, heads, head_dim) -> Schedule:
             computed[r, i] = tuple(done)
             if i < P - 1:
                 carried = zigzag_alive(P, o, i + 1)
+                if direct and o >= 1 and not _direct_carries_low(P, o, r):
+                    carried = tuple(a for a in carried if a != o)
+                if direct and r >= 1 and i == P - r - 1:
+                    if (r + 1) % P == 0:       # host 0 is the ring successor: one message
+                        carried = (r,) + tuple(a for a in carried if a != r)
+                    else:
+                        plan.sends[r].append(MsgPlan(r, 0, MsgKind.Q_BLOCK, (r,),
+                                                     q_elements(c, heads, head_dim)))
                 plan.sends[r].append(MsgPlan(r, (r + 1) % P, MsgKind.Q_BLOCK, carried,
                                              q_elements(len(carried) * c, heads, head_dim)))
             if i >= 2:
@@ -272,12 +342,20 @@ def build_zigzag_token_ring(ranks, seq_len, heads, head_dim) -> Schedule:
     for r in range(P):
         ids = computed[r, P - 1]
         final.sends[r].append(MsgPlan(r, (r + 1) % P, MsgKind.OUT_LSE, ids, len(ids) * oe))
-    return _wire_merges(Schedule("zigzag-token-ring", P, heads, head_dim, True, part, chunks,
-                                 steps, final))
+    return _wire_merges(Schedule(kind, P, heads, head_dim, True, part, chunks, steps, final))
 
 
-def build_schedule(kind: str, ranks, seq_len, heads, head_dim, causal=None) -> Schedule:
-    """Name-based front door: "ring" | "token-ring" | "zigzag-token-ring"."""
+def build_schedule(kind: str, ranks, seq_len, heads, head_dim, causal=None,
+                   nodes: int = 1) -> Schedule:
+    """Name-based front door: "ring" | "token-ring" | "zigzag-token-ring" |
+    "hybrid" (``nodes`` must divide ``ranks``) | "zigzag-token-ring-direct"
+    (non-reference Q routing, see ``build_zigzag_token_ring``)."""
+    if kind == "hybrid":
+        if causal:
+            raise ConfigError("hybrid is non-causal; use zigzag-token-ring")
+        if nodes < 1 or ranks % nodes:
+            raise ConfigError(f"nodes must divide ranks (got ranks={ranks}, nodes={nodes})")
+        return build_hybrid(nodes, ranks // nodes, seq_len, heads, head_dim)
     if kind == "ring":
         return build_ring_attention(ranks, seq_len, heads, head_dim, bool(causal))
     if kind == "token-ring":
@@ -288,6 +366,10 @@ def build_schedule(kind: str, ranks, seq_len, heads, head_dim, causal=None) -> S
         if causal is False:
             raise ConfigError("zigzag-token-ring is causal")
         return build_zigzag_token_ring(ranks, seq_len, heads, head_dim)
+    if kind == "zigzag-token-ring-direct":
+        if causal is False:
+            raise ConfigError("zigzag-token-ring-direct is causal")
+        return build_zigzag_token_ring(ranks, seq_len, heads, head_dim, route="direct")
     raise ConfigError(f"unknown schedule kind {kind!r}")
 
 

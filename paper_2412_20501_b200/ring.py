@@ -62,8 +62,8 @@ class RankStep:
     q_ids: tuple             # q chunks computed this step
     kv_ids: tuple            # local kv chunks used
     accumulate: bool | None
-    send_q: tuple | None     # (dst, ids)
-    recv_q: tuple | None     # (src, ids)   -> layout of the next step's buffer
+    send_q: list             # [(dst, ids, from_home)]  from_home: rows of the local shard
+    recv_q: list             # [(src, ids)]  union (start order) = next step's buffer layout
     send_out: tuple | None   # (dst, ids)   rows from the previous step's output
     recv_out: list           # [(src, ids)]  to merge after this step's comm
 
@@ -72,18 +72,26 @@ def compile_rank(sched, rank: int) -> list:
     """This rank's step program, derived from the schedule's plans."""
     P = sched.ranks
     plans = sched.all_plans()
-    layout = tuple(cid for cid in (c.id for c in sorted(
-        (c for c in sched.chunks if c.home == rank), key=lambda c: c.start)))
+    home = tuple(c.id for c in sorted((c for c in sched.chunks if c.home == rank),
+                                      key=lambda c: c.start))
+    layout = home
+    start = {c.id: c.start for c in sched.chunks}
     prog = []
     for i, plan in enumerate(plans):
         g = group_computes(sched, plan.computes[rank])
         if g is None:
             raise ScheduleError(f"step {i} rank {rank}: compute set not expressible as one launch")
         q_ids, kv_ids, acc = g
-        send_q = send_out = recv_q = None
+        send_q, recv_q, send_out = [], [], None
         for m in plan.sends[rank]:
             if m.kind is MsgKind.Q_BLOCK:
-                send_q = (m.dst, tuple(m.chunk_ids))
+                ids = tuple(m.chunk_ids)
+                if all(a in layout for a in ids):
+                    send_q.append((m.dst, ids, i == 0))
+                elif all(a in home for a in ids):
+                    send_q.append((m.dst, ids, True))      # kept at its origin (direct route)
+                else:
+                    raise ScheduleError(f"step {i} rank {rank}: cannot send q chunks {ids}")
             elif m.kind is MsgKind.OUT_LSE:
                 send_out = (m.dst, tuple(m.chunk_ids))
             else:
@@ -94,15 +102,15 @@ def compile_rank(sched, rank: int) -> list:
                 if m.dst != rank:
                     continue
                 if m.kind is MsgKind.Q_BLOCK:
-                    recv_q = (src, tuple(m.chunk_ids))
+                    recv_q.append((src, tuple(m.chunk_ids)))
                 elif m.kind is MsgKind.OUT_LSE:
                     recv_out.append((src, tuple(m.chunk_ids)))
         for a in q_ids:
             if a not in layout:
                 raise ScheduleError(f"step {i} rank {rank}: q chunk {a} not resident")
         prog.append(RankStep(i, layout, q_ids, kv_ids, acc, send_q, recv_q, send_out, recv_out))
-        if recv_q is not None:
-            layout = recv_q[1]
+        if recv_q:
+            layout = tuple(sorted((a for _, ids in recv_q for a in ids), key=start.get))
     return prog
 
 
@@ -123,12 +131,14 @@ class TokenRingAttention:
     """
 
     def __init__(self, seq_len, heads, head_dim, causal=True, group=None, ops=None,
-                 device=None, record_timeline=False, transport="nccl"):
+                 device=None, record_timeline=False, transport="nccl", route="ring"):
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if route != "ring" and not causal:
+            raise ConfigError("route='direct' applies to the causal zigzag schedule only")
         if causal:
-            self.sched = build_zigzag_token_ring(self.P, seq_len, heads, head_dim)
+            self.sched = build_zigzag_token_ring(self.P, seq_len, heads, head_dim, route=route)
         else:
             self.sched = build_token_ring(self.P, seq_len, heads, head_dim)
         self.causal = causal
@@ -137,6 +147,7 @@ class TokenRingAttention:
         self.local_rows = self.part.owned_tokens(self.rank)
         self.c = self.sched.chunks[0].tokens
         self.prog = compile_rank(self.sched, self.rank)
+        self._layouts = {}
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.ops = ops if ops is not None else CudaOps(device)
@@ -185,13 +196,15 @@ class TokenRingAttention:
     # send is a cudaMemcpyAsync straight into the peer's buffer on this rank's
     # copy stream -- copy engines, no SMs taken from the attention kernel --
     # followed by a release store to the peer's sequence flag.
-    #   flags[0] q_ready : highest step whose Q for me has landed
+    #   flags[0]   (unused)
     #   flags[1] q_free  : highest step whose traveling-Q slot I am done with
     #   flags[2] o_ready : highest step whose returned OUT for me has landed
     #   flags[3] o_free  : highest step whose returned OUT I have merged
+    #   flags[4+s] q_ready from s: highest step whose Q from rank s has landed
+    #              (one per source: the direct route has two Q senders per step)
     def _ipc_setup(self):
         from torch.multiprocessing.reductions import reduce_tensor
-        self.flags = torch.zeros(8, dtype=torch.int64, device=self.device)
+        self.flags = torch.zeros(4 + self.P, dtype=torch.int64, device=self.device)
         mine = [reduce_tensor(t) for t in (self.qbuf[0], self.qbuf[1], self.out_recv,
                                            self.lse_recv, self.flags)]
         everyone = [None] * self.P
@@ -213,6 +226,7 @@ class TokenRingAttention:
         cs = self.copy_stream
         # initial conditions of this call, visible to every peer before anyone sends
         self.flags[:4] = torch.tensor([base - 1, base, base - 1, base + 1], dtype=torch.int64)
+        self.flags[4:] = base - 1
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
         self.ops.init_(self.acc_out, self.acc_lse)
@@ -220,8 +234,9 @@ class TokenRingAttention:
         ev_comp, ev_out_sent = {}, {}
         for st in self.prog:
             i = st.step
-            if i >= 1 and (st.q_ids or st.send_q is not None):
-                kernels.flag_wait_(self.flags[0:1], base + i, cur)       # Q_i has landed
+            if i >= 1 and (st.q_ids or st.send_q):
+                for src, _ in self.prog[i - 1].recv_q:                  # Q_i has landed
+                    kernels.flag_wait_(self.flags[4 + src:5 + src], base + i, cur)
             if i >= 1 and self.prog[i - 1].recv_out:
                 # OUT sent to me at step i-1 has landed: merge it, free the buffer
                 kernels.flag_wait_(self.flags[2:3], base + i - 1, cur)
@@ -234,13 +249,15 @@ class TokenRingAttention:
             cur_q = self.qbuf[i % 2] if i > 0 else q_loc
             ev_q = torch.cuda.Event()
             ev_q.record(cur)
-            if st.send_q is not None:
-                dst, ids = st.send_q
-                a, b = _rows(st.q_layout, ids, c)
+            if st.send_q:
                 cs.wait_event(ev_q)
+            for dst, ids, from_home in st.send_q:
+                src_buf, src_layout = (q_loc, local_layout) if from_home else (cur_q, st.q_layout)
+                a, b = _rows(src_layout, ids, c)
+                d0, d1 = _rows(self._next_layout(dst, i), ids, c)
                 kernels.flag_wait_(self.peer[dst][4][1:2], base + i - 1, cs)   # peer slot free
-                kernels.copy_(self.peer[dst][(i + 1) % 2][: b - a], cur_q[a:b], cs)
-                kernels.flag_set_(self.peer[dst][4][0:1], base + i + 1, cs)
+                kernels.copy_(self.peer[dst][(i + 1) % 2][d0:d1], src_buf[a:b], cs)
+                kernels.flag_set_(self.peer[dst][4][4 + rank:5 + rank], base + i + 1, cs)
             if st.send_out is not None:
                 dst, ids = st.send_out
                 a, b = _rows(self.prog[i - 1].q_layout, ids, c)
@@ -323,12 +340,14 @@ class TokenRingAttention:
                 self._merge_returned(pending_out, local_layout)
             sends, recvs = [], []
             cur = self.qbuf[i % 2] if i > 0 else q_loc
-            if st.send_q is not None:
-                a, b = _rows(st.q_layout, st.send_q[1], c)
-                sends.append((st.send_q[0], cur[a:b]))
-            if st.recv_q is not None:
-                n = len(st.recv_q[1]) * c
-                recvs.append((st.recv_q[0], self.qbuf[(i + 1) % 2][:n]))
+            for dst, ids, from_home in st.send_q:
+                src_buf, src_layout = (q_loc, local_layout) if from_home else (cur, st.q_layout)
+                a, b = _rows(src_layout, ids, c)
+                sends.append((dst, src_buf[a:b]))
+            nxt = self._next_layout(rank, i) if st.recv_q else ()
+            for src, ids in st.recv_q:
+                a, b = _rows(nxt, ids, c)
+                recvs.append((src, self.qbuf[(i + 1) % 2][a:b]))
             if st.send_out is not None:
                 prev_layout = self.prog[i - 1].q_layout
                 a, b = _rows(prev_layout, st.send_out[1], c)
@@ -380,6 +399,18 @@ class TokenRingAttention:
         if pending_out:
             self._merge_returned(pending_out, local_layout)
         return Partial(self.acc_out, self.acc_lse)
+
+    def _next_layout(self, dst, step):
+        """Row layout of ``dst``'s traveling-Q buffer after the messages of
+        ``step`` land (all Q chunks sent to it that step, in start order) --
+        what its own ``compile_rank`` derives."""
+        key = (dst, step)
+        if key not in self._layouts:
+            plan = self.sched.all_plans()[step]
+            ids = [a for src in range(self.P) for m in plan.sends[src]
+                   if m.dst == dst and m.kind is MsgKind.Q_BLOCK for a in m.chunk_ids]
+            self._layouts[key] = tuple(sorted(ids, key=lambda a: self.sched.chunks[a].start))
+        return self._layouts[key]
 
     def step_flops(self, st) -> int:
         """Algorithmic flops of one step's launch (ref engine.py:170-173)."""

@@ -176,9 +176,15 @@ SCHED_SMALL += [
     ("token-ring", 4, 24000, 32, 128, False),
     ("ring", 4, 24000, 32, 128, False),
 ]
+# hybrid (TokenRing inside a node, KV rotation across nodes): args carry nodes
+SCHED_SMALL += [("hybrid", m * g, 16 * m * g, 2, 4, False, m)
+                for m, g in ((1, 1), (1, 4), (2, 1), (2, 2), (2, 4), (3, 2), (4, 2), (2, 8))]
+SCHED_SMALL += [("hybrid", 16, 131072, 32, 128, False, 2)]
 
 
-def build(kind, p, s, h, d, causal):
+def build(kind, p, s, h, d, causal, nodes=1):
+    if kind == "hybrid":
+        return engine.build_hybrid(nodes, p // nodes, s, h, d)
     if kind == "ring":
         return engine.build_ring_attention(p, s, h, d, causal=causal)
     if kind == "token-ring":
@@ -188,12 +194,13 @@ def build(kind, p, s, h, d, causal):
 
 def schedules():
     out = []
-    for kind, p, s, h, d, causal in SCHED_SMALL:
-        sc = build(kind, p, s, h, d, causal)
+    for args in SCHED_SMALL:
+        kind, p, s, h, d, causal = args[:6]
+        sc = build(*args)
         tr = engine.trace_from_schedule(sc)
         vol = engine.comm_volume(sc)
         out.append({
-            "args": [kind, p, s, h, d, causal],
+            "args": list(args),
             "schedule": canon(sc),
             "ranges": [list(map(list, sc.partition.ranges(r))) for r in range(p)],
             "causal_work": list(partition.causal_work_count(sc.partition)),
@@ -217,13 +224,16 @@ EXEC_CASES = [
     # bf16-rounded inputs at kernel head dims, for the GPU executor fixtures
     ("zz_p4_bf16_d128", "zigzag-token-ring", 4, 1024, 2, 128, True, 31, True),
     ("tr_p2_bf16_d64", "token-ring", 2, 512, 2, 64, False, 32, True),
+    ("hy_2x2", "hybrid", 4, 64, 2, 8, False, 12, False, 2),
+    ("hy_2x4_bf16_d128", "hybrid", 8, 512, 2, 128, False, 33, True, 2),
+    ("hy_3x2_bf16_d64", "hybrid", 6, 768, 2, 64, False, 34, True, 3),
 ]
 
 
 def exec_cases():
     arrs, meta = {}, []
-    for name, kind, p, s, h, d, causal, seed, bf in EXEC_CASES:
-        sc = build(kind, p, s, h, d, causal)
+    for name, kind, p, s, h, d, causal, seed, bf, *nodes in EXEC_CASES:
+        sc = build(kind, p, s, h, d, causal, *nodes)
         q, k, v = rng.attention_inputs(seed, s, h, d)
         if bf:
             q, k, v = to_bf16_f64(q), to_bf16_f64(k), to_bf16_f64(v)
@@ -234,7 +244,8 @@ def exec_cases():
         dense = ringsim.dense_attention_oracle(q, k, v, causal=causal)
         arrs[f"{name}__dense_out"] = dense.out
         arrs[f"{name}__dense_lse"] = dense.lse
-        meta.append({"name": name, "args": [kind, p, s, h, d, causal], "seed": seed, "bf16": bf})
+        meta.append({"name": name, "args": [kind, p, s, h, d, causal, *nodes], "seed": seed,
+                     "bf16": bf})
     return arrs, meta
 
 

@@ -38,7 +38,9 @@ def test_volume_matches_reference_output():
     (lambda d: d["problem"].update(dtype="bf16"), "unknown key"),
     (lambda d: d["problem"].update(causal=False), "requires causal=true"),
     (lambda d: d["problem"].update(seq_len=60), "2P must divide seq_len"),
-    (lambda d: d["schedule"].update(kind="hybrid"), "not part of the B200 path"),
+    (lambda d: d["schedule"].update(kind="hybrid"), "hybrid schedule requires causal=false"),
+    (lambda d: (d["schedule"].update(kind="hybrid"), d["problem"].update(causal=False),
+                d["parallel"].update(nodes=3)), "nodes must divide ranks"),
     (lambda d: d["schedule"].update(kind="bogus"), "unknown schedule kind"),
     (lambda d: d.update(topology={"kind": "torus"}), "unknown topology kind"),
     (lambda d: d.update(timing={"efficiency": 1.5}), "efficiency"),

@@ -31,37 +31,34 @@ def test_execute_matches_reference_golden(golden_execute):
     import paper_2412_20501_b200 as tr
     meta, arr = golden_execute
     for m in meta:
-        kind, p, s, h, d, causal = m["args"]
-        sc = tr.build_schedule(kind, p, s, h, d, causal if kind == "ring" else None)
+        kind, p, s, h, d, causal = m["args"][:6]
+        nodes = m["args"][6] if len(m["args"]) > 6 else 1
+        sc = tr.build_schedule(kind, p, s, h, d, causal if kind == "ring" else None, nodes=nodes)
         q, k, v = splitmix.attention_inputs(m["seed"], s, h, d)
         qb, kb, vb = (splitmix.to_bf16_f64(x) for x in (q, k, v))
         outs, trace = tr.execute(sc, dev(qb), dev(kb), dev(vb))
         torch.cuda.synchronize()
-        ref = osch.execute(osch.zigzag_token_ring(p, s, h, d) if kind == "zigzag-token-ring" else
-                           osch.token_ring(p, s, h, d) if kind == "token-ring" else
-                           osch.ring(p, s, h, d, causal), qb, kb, vb)
+        ref = osch.execute(osch.by_name(*m["args"]), qb, kb, vb)
         for r in range(p):
             if m["bf16"]:       # golden itself was computed on bf16-rounded inputs
                 close(outs[r].out, outs[r].lse, arr[f"{m['name']}__out{r}"],
                       arr[f"{m['name']}__lse{r}"], m["name"])
             close(outs[r].out, outs[r].lse, ref[r][0], ref[r][1], m["name"])
-        assert sum(c.flops for c in trace.computes) == osch.flops(
-            osch.zigzag_token_ring(p, s, h, d) if kind == "zigzag-token-ring" else
-            osch.token_ring(p, s, h, d) if kind == "token-ring" else
-            osch.ring(p, s, h, d, causal), h, d)
+        assert sum(c.flops for c in trace.computes) == osch.flops(osch.by_name(*m["args"]), h, d)
 
 
-@pytest.mark.parametrize("P,S,H,D", [(2, 4096, 8, 64), (4, 4096, 4, 128), (8, 8192, 2, 128),
-                                     (1, 2048, 4, 128)])
-def test_execute_zigzag_vs_dense_oracle(P, S, H, D):
+@pytest.mark.parametrize("P,S,H,D,route", [(2, 4096, 8, 64, "ring"), (4, 4096, 4, 128, "ring"),
+                                           (8, 8192, 2, 128, "ring"), (1, 2048, 4, 128, "ring"),
+                                           (8, 8192, 2, 128, "direct"), (5, 5120, 2, 64, "direct")])
+def test_execute_zigzag_vs_dense_oracle(P, S, H, D, route):
     import paper_2412_20501_b200 as tr
     q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(3 + P, S, H, D))
-    sc = tr.build_zigzag_token_ring(P, S, H, D)
+    sc = tr.build_zigzag_token_ring(P, S, H, D, route=route)
     outs, _ = tr.execute(sc, dev(q), dev(k), dev(v))
     merged = tr.global_reorder(outs, sc.partition)
     torch.cuda.synchronize()
     ref_o, ref_l = ok.dense_attention(q, k, v, causal=True)
-    close(merged.out, merged.lse, ref_o, ref_l, f"zigzag P={P}")
+    close(merged.out, merged.lse, ref_o, ref_l, f"zigzag P={P} {route}")
 
 
 def test_config1_token_ring_p2():

@@ -29,7 +29,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, S, H, D, causal, calls, q_out):
+def _worker(rank, world, port, S, H, D, causal, calls, q_out, route):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -38,7 +38,7 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out):
         from paper_2412_20501_b200 import rng
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
-                                    transport="ipc")
+                                    transport="ipc", route=route)
         q, k, v = rng.local_inputs(21, runner.part, rank, H, D)
         for _ in range(calls):            # repeated calls exercise the flag bases
             res = runner(q, k, v)
@@ -49,13 +49,14 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,S,H,D,causal", [(2, 2048, 2, 128, True), (4, 4096, 2, 128, True),
-                                               (2, 1024, 2, 64, False)])
-def test_token_ring_ipc(world, S, H, D, causal):
+@pytest.mark.parametrize("world,S,H,D,causal,route", [
+    (2, 2048, 2, 128, True, "ring"), (4, 4096, 2, 128, True, "ring"), (2, 1024, 2, 64, False, "ring"),
+    (4, 4096, 2, 128, True, "direct")])
+def test_token_ring_ipc(world, S, H, D, causal, route):
     ctx = mp.get_context("spawn")
     q_out = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, S, H, D, causal, 3, q_out))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, S, H, D, causal, 3, q_out, route))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -103,18 +103,14 @@ def test_merge_golden(golden_merge):
     assert np.array_equal(o, np.array([[[2.0, -0.75]]])) and l[0, 0] == np.log(2)
 
 
-def _build(kind, p, s, h, d, causal):
-    if kind == "ring":
-        return osch.ring(p, s, h, d, causal)
-    if kind == "token-ring":
-        return osch.token_ring(p, s, h, d)
-    return osch.zigzag_token_ring(p, s, h, d)
+def _build(kind, p, s, h, d, causal, nodes=1):
+    return osch.by_name(kind, p, s, h, d, causal, nodes)
 
 
 def test_schedules_golden(golden_schedules):
     for g in golden_schedules:
-        kind, p, s, h, d, causal = g["args"]
-        sc = _build(kind, p, s, h, d, causal)
+        kind, p, s, h, d, causal = g["args"][:6]
+        sc = _build(*g["args"])
         assert sc == g["schedule"], g["args"]
         rr = osch.ranges_of(sc, s)
         assert [list(map(list, x)) for x in rr] == g["ranges"]
@@ -125,10 +121,10 @@ def test_schedules_golden(golden_schedules):
 def test_execute_golden(golden_execute):
     meta, arr = golden_execute
     for m in meta:
-        kind, p, s, h, d, causal = m["args"]
+        kind, p, s, h, d, causal = m["args"][:6]
         if s * h * d > 300_000:
             continue       # large fixtures are for the GPU tests
-        sc = _build(kind, p, s, h, d, causal)
+        sc = _build(*m["args"])
         q, k, v = splitmix.attention_inputs(m["seed"], s, h, d)
         if m["bf16"]:
             q, k, v = (splitmix.to_bf16_f64(x) for x in (q, k, v))

@@ -27,14 +27,15 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, S, H, D, causal, seed, result_q):
+def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from cpu_ops import OracleOps
         from paper_2412_20501_b200.ring import TokenRingAttention
-        runner = TokenRingAttention(S, H, D, causal=causal, ops=OracleOps(), device="cpu")
+        runner = TokenRingAttention(S, H, D, causal=causal, ops=OracleOps(), device="cpu",
+                                    route=route)
         q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(seed, S, H, D))
         rng = runner.part.ranges(rank)
         loc = [torch.as_tensor(opart.gather(x, rng), dtype=torch.float32).to(torch.bfloat16)
@@ -45,13 +46,16 @@ def _worker(rank, world, port, S, H, D, causal, seed, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,S,H,D,causal", [(2, 64, 2, 8, True), (4, 128, 2, 8, True),
-                                               (2, 48, 2, 8, False), (3, 96, 1, 8, True)])
-def test_token_ring_gloo(world, S, H, D, causal):
+@pytest.mark.parametrize("world,S,H,D,causal,route", [
+    (2, 64, 2, 8, True, "ring"), (4, 128, 2, 8, True, "ring"), (2, 48, 2, 8, False, "ring"),
+    (3, 96, 1, 8, True, "ring"),
+    # non-reference NVSwitch-aware Q routing: same computes, different messages
+    (4, 128, 2, 8, True, "direct"), (5, 160, 1, 8, True, "direct")])
+def test_token_ring_gloo(world, S, H, D, causal, route):
     ctx = mp.get_context("spawn")
     q_ = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, S, H, D, causal, 11, q_))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, S, H, D, causal, 11, q_, route))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -25,14 +25,15 @@ def canon(s):
             "final": plan(s.final_phase) if s.final_phase else None}
 
 
-def build(kind, p, s, h, d, causal):
-    return engine.build_schedule(kind, p, s, h, d, causal if kind == "ring" else None)
+def build(kind, p, s, h, d, causal, nodes=1):
+    return engine.build_schedule(kind, p, s, h, d, causal if kind == "ring" else None,
+                                 nodes=nodes)
 
 
 def test_schedules_bit_exact(golden_schedules):
     for g in golden_schedules:
-        kind, p, s, h, d, causal = g["args"]
-        sc = build(kind, p, s, h, d, causal)
+        kind, p, s, h, d, causal = g["args"][:6]
+        sc = build(*g["args"])
         assert canon(sc) == g["schedule"], g["args"]
         assert [list(map(list, sc.partition.ranges(r))) for r in range(p)] == g["ranges"]
         assert list(partition.causal_work_count(sc.partition)) == g["causal_work"]
@@ -110,3 +111,33 @@ def test_rank_programs_cover_all_pairs_once():
                             seen[(a, b)] = seen.get((a, b), 0) + 1
         want = {(a, b) for a in range(2 * P) for b in range(2 * P) if a >= b}
         assert set(seen) == want and all(v == 1 for v in seen.values())
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 8])
+def test_direct_route_same_computes_fewer_q_bytes(P):
+    """NVSwitch-aware Q routing (a non-reference schedule):
+    identical computes and merges at every rank and step, Q chunk-hops
+    reduced from (P-1)(2P-1) to (P-1)(2P-1) - (P-1)(P-2)/2, and every
+    compiled rank program still finds each q chunk it computes or forwards."""
+    from paper_2412_20501_b200.ring import compile_rank
+    c, H, D = 16, 2, 8
+    ref = engine.build_zigzag_token_ring(P, 2 * P * c, H, D)
+    dr = engine.build_schedule("zigzag-token-ring-direct", P, 2 * P * c, H, D)
+    assert dr.kind == "zigzag-token-ring-direct" and dr.n_steps == ref.n_steps
+    for a, b in zip(ref.all_plans(), dr.all_plans()):
+        assert a.computes == b.computes and a.merges == b.merges
+        for r in range(P):
+            assert ([m for m in a.sends[r] if m.kind is engine.MsgKind.OUT_LSE]
+                    == [m for m in b.sends[r] if m.kind is engine.MsgKind.OUT_LSE])
+
+    def q_hops(s):
+        return sum(n for (_, _, k), n in engine.comm_volume(s).entries.items()
+                   if k is engine.MsgKind.Q_BLOCK) // (c * H * D)
+    assert q_hops(ref) == (P - 1) * (2 * P - 1)
+    assert q_hops(dr) == (P - 1) * (2 * P - 1) - (P - 1) * (P - 2) // 2
+    for r in range(P):
+        compile_rank(dr, r)
+    if P == 2:
+        assert canon(dr)["steps"] == canon(ref)["steps"]
+    with pytest.raises(ConfigError):
+        engine.build_zigzag_token_ring(P, 2 * P * c, H, D, route="mesh")
