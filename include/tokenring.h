@@ -72,11 +72,14 @@ int tr_attention_block(const void* q, const void* k, const void* v, void* out, f
  * local k/v buffer, in one launch.  Every q segment attends to the union of the
  * kv segments (causal: by position).  out/lse rows follow q's local rows;
  * lse has row stride tq_total.  Rows of q not covered by a segment are left
- * untouched. */
+ * untouched.  out_dtype TR_DTYPE_BF16 writes a bf16 block result;
+ * TR_DTYPE_F32 writes float32 rows, so a block that is the first contribution
+ * to a float32 accumulator (engine.py:585-589 merging into Partial.empty)
+ * lands in it directly, with no bf16 round trip, init or merge pass. */
 int tr_attention_segments(const void* q, const void* k, const void* v, void* out, float* lse,
                           int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
                           const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
-                          int32_t n_kv, int32_t causal, void* stream);
+                          int32_t n_kv, int32_t causal, int32_t out_dtype, void* stream);
 
 /* kernels.merge_state, in place on a float32 accumulator:
  *   acc <- merge(acc, blk)     (ref _kernels.pyx:68-102)

@@ -53,7 +53,7 @@ def _declare(lib):
     lib.tr_attention_block.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32, i32, i64, i64, vp]
     lib.tr_attention_segments.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32,
                                           ctypes.POINTER(Segment), i32,
-                                          ctypes.POINTER(Segment), i32, i32, vp]
+                                          ctypes.POINTER(Segment), i32, i32, i32, vp]
     lib.tr_merge_state.argtypes = [vp, vp, vp, i32, vp, i64, i32, i32, i64, i64, vp, vp]
     lib.tr_partial_init.argtypes = [vp, vp, i64, i32, i32, vp]
     lib.tr_splitmix_bf16.argtypes = [ctypes.c_uint64, i64, i64, ctypes.c_double,

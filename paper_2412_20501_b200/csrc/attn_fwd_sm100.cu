@@ -45,7 +45,7 @@ struct AttnCfg {
   static constexpr uint32_t IDESC_PV = idesc_bf16(128, D, true);
   static constexpr float RESCALE_LOG2 = 8.0f;
 #ifndef TR_POLY_MOD
-#define TR_POLY_MOD 4
+#define TR_POLY_MOD 6
 #endif
   static constexpr int POLY_MOD = TR_POLY_MOD;   // 1 of every POLY_MOD exp2 pairs on the FMA pipe
 };
@@ -386,7 +386,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     // ---------------------------------------------------------- epilogue
     const bool row_ok = row_in_seg < Q.rows;
     const int64_t grow = Q.row0 + row_in_seg;
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + (grow * p.heads + head) * D;
+    const int64_t oidx = (grow * p.heads + head) * D;
     if (ntiles > 0) {
       mbar_wait(&o_done[h], 0);
       tc_fence_after();
@@ -402,12 +402,23 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         #pragma unroll
         for (int i = 0; i < 32; ++i) u[i] = 0u;
       }
+      if (p.out_f32) {
+        // float32 rows straight into an (empty) accumulator: no bf16 round trip
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oidx + cc * 32);
+          #pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(u[4 * i]) * inv, __uint_as_float(u[4 * i + 1]) * inv,
+                                 __uint_as_float(u[4 * i + 2]) * inv, __uint_as_float(u[4 * i + 3]) * inv);
+        }
+        continue;
+      }
       uint32_t pk[16];
       #pragma unroll
       for (int i = 0; i < 16; ++i)
         pk[i] = pack_bf16x2(__uint_as_float(u[2 * i]) * inv, __uint_as_float(u[2 * i + 1]) * inv);
       if (row_ok) {
-        uint4* dst = reinterpret_cast<uint4*>(out + cc * 32);
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oidx + cc * 32);
         #pragma unroll
         for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       }

@@ -66,11 +66,15 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(const __nv_bfloat16* __r
     }
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
-  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int d = lane + 32 * i;
-    if (d < D) out[row * ld + head * D + d] = __float2bfloat16_rn(acc[i] * inv);
+    if (d >= D) continue;
+    if (p.out_f32)
+      reinterpret_cast<float*>(p.out)[row * ld + head * D + d] = acc[i] * inv;
+    else
+      reinterpret_cast<__nv_bfloat16*>(p.out)[row * ld + head * D + d] =
+          __float2bfloat16_rn(acc[i] * inv);
   }
   if (lane == 0) p.lse[head * p.lse_stride + row] = l > 0.f ? m + logf(l) : -INFINITY;
 }

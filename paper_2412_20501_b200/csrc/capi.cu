@@ -45,7 +45,9 @@ static int check_segments(const tr_segment* segs, int n, int64_t total, const ch
 static int run_segments(const void* q, const void* k, const void* v, void* out, float* lse,
                         int64_t tq_total, int64_t tk_total, int heads, int head_dim,
                         const tr_segment* qs, int nq, const tr_segment* ks, int nk, int causal,
-                        cudaStream_t s) {
+                        int out_dtype, cudaStream_t s) {
+  if (out_dtype != TR_DTYPE_BF16 && out_dtype != TR_DTYPE_F32)
+    return fail(TR_ERR_CONFIG, "out_dtype must be TR_DTYPE_BF16 or TR_DTYPE_F32");
   if (heads < 1 || head_dim < 1 || tq_total < 0 || tk_total < 0)
     return fail(TR_ERR_DIMENSION, "heads, head_dim must be >= 1 and token counts >= 0");
   int rc;
@@ -65,6 +67,7 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   plan.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(head_dim)));
   plan.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(head_dim)));
   plan.out = out;
+  plan.out_f32 = out_dtype == TR_DTYPE_F32 ? 1 : 0;
   plan.lse = lse;
   plan.tile_prefix[0] = 0;
   for (int i = 0; i < plan.nq; ++i)
@@ -97,15 +100,15 @@ int tr_attention_block(const void* q, const void* k, const void* v, void* out, f
   tr_segment qs{0, tq, q_offset};
   tr_segment ks{0, tk, k_offset};
   return run_segments(q, k, v, out, lse, tq, tk, heads, head_dim, &qs, 1, &ks, 1,
-                      mask_kind == TR_MASK_CAUSAL, s);
+                      mask_kind == TR_MASK_CAUSAL, TR_DTYPE_BF16, s);
 }
 
 int tr_attention_segments(const void* q, const void* k, const void* v, void* out, float* lse,
                           int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
                           const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
-                          int32_t n_kv, int32_t causal, void* stream) {
+                          int32_t n_kv, int32_t causal, int32_t out_dtype, void* stream) {
   return run_segments(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
-                      n_kv, causal, static_cast<cudaStream_t>(stream));
+                      n_kv, causal, out_dtype, static_cast<cudaStream_t>(stream));
 }
 
 int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t blk_dtype,

@@ -23,6 +23,7 @@ struct AttnPlan {
   int32_t heads;
   float scale;       // 1/sqrt(D)
   float scale_log2;  // log2(e)/sqrt(D)
+  int32_t out_f32;   // out is float32 (an empty accumulator) instead of bf16
   void* out;
   float* lse;
 };

@@ -525,8 +525,9 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list
     for c in ch:
         q_res[c.home].add(c.id)
         kv_res[c.home].add(c.id)
-    acc_out = torch.zeros(shape, dtype=torch.float32, device=dev)
-    acc_lse = torch.full((H, S), float("-inf"), dtype=torch.float32, device=dev)
+    acc_out = torch.empty(shape, dtype=torch.float32, device=dev)
+    acc_lse = torch.empty((H, S), dtype=torch.float32, device=dev)
+    fresh = {c.id for c in ch}      # chunks whose accumulator rows are still Partial.empty
     stage_out = [torch.empty(shape, dtype=torch.bfloat16, device=dev) for _ in range(2)]
     stage_lse = [torch.empty((H, S), dtype=torch.float32, device=dev) for _ in range(2)]
     stash = {r: None for r in range(P)}       # rank -> (stage index, chunk ids)
@@ -535,6 +536,9 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list
 
     def merge_rows(cid, buf):
         c = ch[cid]
+        if cid in fresh:           # first contribution: empty accumulator rows
+            kernels.partial_init_(acc_out[c.start:c.stop], acc_lse[:, c.start:c.stop])
+            fresh.discard(cid)
         kernels.merge_state_(acc_out[c.start:c.stop], acc_lse[:, c.start:c.stop],
                              stage_out[buf][c.start:c.stop], stage_lse[buf][:, c.start:c.stop])
 
@@ -601,13 +605,19 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list
             if timeline is not None:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
+            # accumulate-only rows that are the chunks' first contribution go
+            # straight into the float32 accumulator (no init, no merge)
+            direct = accumulate and all(a in fresh and ch[a].home == r for a in qs)
             kernels.attention_segments(q, k, v, q_segs, kv_segs, sched.causal,
-                                       stage_out[buf], stage_lse[buf])
+                                       acc_out if direct else stage_out[buf],
+                                       acc_lse if direct else stage_lse[buf])
             if timeline is not None:
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev1.record()
                 timeline.append((step, r, ev0, ev1))
-            if accumulate:
+            if direct:
+                fresh.difference_update(qs)
+            elif accumulate:
                 for a in sorted(qs):
                     if ch[a].home != r:
                         raise ScheduleError(f"step {step} rank {r}: accumulate for chunk {a} "
@@ -634,6 +644,10 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list
                 else:
                     in_flight.append((r, m.dst, m.kind, tuple(m.chunk_ids), outgoing[r]))
                 trace.messages.append(MsgRecord(step, r, m.dst, m.kind, m.payload_elements))
+    for cid in sorted(fresh):      # rows nobody contributed to stay Partial.empty
+        c = ch[cid]
+        kernels.partial_init_(acc_out[c.start:c.stop], acc_lse[:, c.start:c.stop])
+    fresh.clear()
     last = sched.n_steps - 1
     for m in in_flight:
         if m[2] is not MsgKind.OUT_LSE:

@@ -92,16 +92,22 @@ def _segs(segs):
 
 def attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse):
     """Every q segment (row0, rows, pos0) against the union of the kv segments
-    in one launch; writes out/lse rows of the q segments only."""
+    in one launch; writes out/lse rows of the q segments only.  ``out`` is a
+    bf16 block buffer, or a float32 accumulator that these rows are the first
+    contribution to (written directly, replacing init + merge)."""
     _check_qkv(q, k, v)
-    _require_cuda("out", out, torch.bfloat16)
+    if not isinstance(out, torch.Tensor) or out.dtype not in (torch.bfloat16, torch.float32):
+        raise DimensionError("out must be a bf16 or float32 tensor")
+    _require_cuda("out", out, out.dtype)
     _require_cuda("lse", lse, torch.float32)
     if out.shape != q.shape or lse.shape != (q.shape[1], q.shape[0]):
         raise DimensionError("out/lse must match q's (T,H,D) / (H,T)")
     qs, ks = _segs(q_segs), _segs(kv_segs)
+    dt = _lib.TR_DTYPE_F32 if out.dtype == torch.float32 else _lib.TR_DTYPE_BF16
     _lib.check(_lib.lib().tr_attention_segments(
         _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
-        q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, _stream(q.device)))
+        q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, dt,
+        _stream(q.device)))
     _count(1)
     return out, lse
 

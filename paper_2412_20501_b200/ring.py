@@ -148,6 +148,12 @@ class TokenRingAttention:
         self.c = self.sched.chunks[0].tokens
         self.prog = compile_rank(self.sched, self.rank)
         self._layouts = {}
+        # Step 0 computes every home chunk with accumulate=True (TokenRing and
+        # zigzag TokenRing alike): those rows are the accumulator's first
+        # contribution, so the kernel writes them into it as float32 -- no
+        # Partial.empty fill, no bf16 block, no merge pass.
+        st0 = self.prog[0]
+        self.direct_first = bool(st0.accumulate) and sorted(st0.q_ids) == sorted(st0.q_layout)
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.ops = ops if ops is not None else CudaOps(device)
@@ -229,7 +235,8 @@ class TokenRingAttention:
         self.flags[4:] = base - 1
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
-        self.ops.init_(self.acc_out, self.acc_lse)
+        if not self.direct_first:
+            self.ops.init_(self.acc_out, self.acc_lse)
         local_layout = self.prog[0].q_layout
         ev_comp, ev_out_sent = {}, {}
         for st in self.prog:
@@ -280,9 +287,13 @@ class TokenRingAttention:
                 kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
                             self.sched.chunks[b].start) for b in st.kv_ids]
                 buf = i % 2
-                self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
-                                   self.obuf[buf], self.lbuf[buf])
-                if st.accumulate:
+                if i == 0 and self.direct_first:
+                    self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                                       self.acc_out, self.acc_lse)
+                else:
+                    self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                                       self.obuf[buf], self.lbuf[buf])
+                if st.accumulate and not (i == 0 and self.direct_first):
                     for a in st.q_ids:
                         r0, r1 = _rows(st.q_layout, (a,), c)
                         l0 = self.part.local_offset(rank, self.sched.chunks[a].start)
@@ -322,7 +333,8 @@ class TokenRingAttention:
                 raise DimensionError(f"{n} shard must have shape {shape}, got {tuple(t.shape)}")
         c, rank = self.c, self.rank
         local_layout = self.prog[0].q_layout
-        self.ops.init_(self.acc_out, self.acc_lse)
+        if not self.direct_first:
+            self.ops.init_(self.acc_out, self.acc_lse)
         pending, pending_out = [], None
         self.timeline = []
         for st in self.prog:
@@ -378,13 +390,15 @@ class TokenRingAttention:
                 if self.record_timeline:
                     ev["attn_start"] = self.ops.event()
                     self.ops.record(ev["attn_start"])
+                first = i == 0 and self.direct_first
                 self.ops.attention(cur, k_loc, v_loc, q_segs, kv_segs, self.causal,
-                                   self.obuf[buf], self.lbuf[buf])
+                                   self.acc_out if first else self.obuf[buf],
+                                   self.acc_lse if first else self.lbuf[buf])
                 if self.record_timeline:
                     ev["attn_end"] = self.ops.event()
                     self.ops.record(ev["attn_end"])
                     ev["attn_flops"] = self.step_flops(st)
-                if st.accumulate:
+                if st.accumulate and not first:
                     for a in st.q_ids:
                         r0, r1 = _rows(st.q_layout, (a,), c)
                         l0 = self.part.local_offset(rank, self.sched.chunks[a].start)

@@ -65,10 +65,13 @@ def test_validation_maps_to_reference_errors(lib):
     segs = (lib.Segment * 1)(lib.Segment(0, 10, 0))
     with pytest.raises(DimensionError):   # segment runs past the 8-row buffer
         lib.check(L.tr_attention_segments(null, null, null, null, null, 8, 8, 1, 64,
-                                          segs, 1, segs, 1, 1, null))
+                                          segs, 1, segs, 1, 1, lib.TR_DTYPE_BF16, null))
     with pytest.raises(ConfigError):
         lib.check(L.tr_attention_segments(null, null, null, null, null, 8, 8, 1, 64,
-                                          segs, 5, segs, 1, 1, null))
+                                          segs, 5, segs, 1, 1, lib.TR_DTYPE_BF16, null))
+    with pytest.raises(ConfigError):       # out dtype other than bf16 / f32
+        lib.check(L.tr_attention_segments(null, null, null, null, null, 8, 8, 1, 64,
+                                          segs, 1, segs, 1, 1, 7, null))
     with pytest.raises(ConfigError):
         lib.check(L.tr_splitmix_bf16(1, -1, 4, -1.0, 1.0, null, null))
 

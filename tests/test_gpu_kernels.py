@@ -124,6 +124,39 @@ def test_segments_zigzag_step0(K):
         check(out[qa:qa + c], lse[:, qa:qa + c], ref_o, ref_l, f"chunk {qi}")
 
 
+@pytest.mark.parametrize("d", [128, 64, 32])
+def test_segments_float32_out(K, d):
+    """out_dtype float32 (first contribution written straight into an
+    accumulator): same rows as the bf16 path before rounding, so within one
+    bf16 ulp of it and tighter to the oracle; uncovered rows untouched."""
+    P, c, h = 2, 320, 2
+    S = 2 * P * c
+    q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(8 + d, S, h, d))
+    segs = [(0, c, 0), (c, c, 3 * c)]
+    rows = np.r_[0:c, 3 * c:4 * c]
+    ql, kl, vl = dev(q[rows]), dev(k[rows]), dev(v[rows])
+    o16 = torch.zeros((2 * c, h, d), dtype=torch.bfloat16, device="cuda")
+    l16 = torch.zeros((h, 2 * c), dtype=torch.float32, device="cuda")
+    o32 = torch.full((2 * c, h, d), 7.0, dtype=torch.float32, device="cuda")
+    l32 = torch.full((h, 2 * c), 7.0, dtype=torch.float32, device="cuda")
+    K.attention_segments(ql, kl, vl, segs, segs, True, o16, l16)
+    K.attention_segments(ql, kl, vl, segs[1:], segs, True, o32, l32)   # chunk 3 only
+    torch.cuda.synchronize()
+    assert torch.all(o32[:c] == 7.0) and torch.all(l32[:, :c] == 7.0)
+    assert torch.equal(l32[:, c:], l16[:, c:])
+    assert torch.equal(o32[c:].to(torch.bfloat16), o16[c:])
+    qa = np.asarray(q[rows])
+    ref_o = np.zeros((c, h, d))
+    ref_l = np.full((h, c), -np.inf)
+    for ka, kpos in ((0, 0), (c, 3 * c)):
+        bo, bl = ok.attention_block(qa[c:], np.asarray(k[rows])[ka:ka + c],
+                                    np.asarray(v[rows])[ka:ka + c], 2, 3 * c, kpos)
+        ref_o, ref_l = ok.merge_state(ref_o, ref_l, bo, bl)
+    err32 = np.abs(o32[c:].double().cpu().numpy() - ref_o).max()
+    err16 = np.abs(o16[c:].double().cpu().numpy() - ref_o).max()
+    assert err32 <= err16 + 1e-6 and err32 <= 5e-3, (err32, err16)
+
+
 def test_merge_golden(K, golden_merge):
     names, arr = golden_merge
     for n in names:
