@@ -232,7 +232,7 @@ def ncu_traffic():
         return None
 
 
-def e2e_pipelined(runner, q, k, v, steps, barrier, world):
+def e2e_pipelined(runner, q, k, v, steps, barrier, allmax):
     """Per step: H2D of that step's q/k/v (pinned host), the TokenRing
     forward, D2H of its bf16 output and lse.  Copies run on their own streams
     (H2D of step i+1 and D2H of step i-1 overlap step i's compute); every
@@ -292,12 +292,7 @@ def e2e_pipelined(runner, q, k, v, steps, barrier, world):
     s, e = run(steps)
     torch.cuda.synchronize()
     barrier()
-    ms = s.elapsed_time(e) / steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    return ms
+    return allmax([s.elapsed_time(e) / steps])[0]
 
 
 def run_ours(a):
@@ -309,9 +304,26 @@ def run_ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # TR_BENCH_SHARED_DEVICE=1: test mode for the multi-rank flow on a one-GPU
+    # box -- every rank on cuda:0, copy-engine transport, gloo for the host
+    # collectives.  Numbers from it are not scaling numbers.
+    shared = os.environ.get("TR_BENCH_SHARED_DEVICE") == "1" and world > 1
+    if shared and a.transport != "ipc":
+        raise SystemExit("TR_BENCH_SHARED_DEVICE=1 needs --transport ipc")
+    dev_index = 0 if shared else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def allmax(vals):
+        if world == 1:
+            return list(vals)
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.tolist()]
 
     from paper_2412_20501_b200 import kernels, rng
     from paper_2412_20501_b200.ring import TokenRingAttention
@@ -336,12 +348,7 @@ def run_ours(a):
         e.record()
         torch.cuda.synchronize()
         barrier()
-        ms = s.elapsed_time(e) / steps
-        if world > 1:
-            t = torch.tensor([ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return allmax([s.elapsed_time(e) / steps])[0]
 
     timelines = []
 
@@ -353,7 +360,7 @@ def run_ours(a):
         step()
     timelines.clear()
     launches0 = kernels.LAUNCHES
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev_index) as clk:
         ms = timed(step, a.steps)
     launches = (kernels.LAUNCHES - launches0) // a.steps * a.steps
     torch.cuda.synchronize()
@@ -371,16 +378,13 @@ def run_ours(a):
     exposed = stall / max(1, len(timelines))
     attn_avg_ms = kern_ms / max(1, nlaunch)
     attn_flops_per_launch = kern_flops / max(1, nlaunch)
-    if world > 1:
-        t = torch.tensor([exposed, attn_avg_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        exposed, attn_avg_ms = (float(x) for x in t.tolist())
+    exposed, attn_avg_ms = allmax([exposed, attn_avg_ms])
 
     # end-to-end through the public API with host buffers
     e2e = None
     if not a.no_e2e:
         e2e_steps = max(2, a.steps)     # pipeline fill/drain amortised over the K steps
-        e2e_ms = e2e_pipelined(runner, q, k, v, e2e_steps, barrier, world)
+        e2e_ms = e2e_pipelined(runner, q, k, v, e2e_steps, barrier, allmax)
         h2d = 3 * q.numel() * 2 * world
         d2h = (q.numel() * 2 + runner.acc_lse.numel() * 4) * world
         e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
@@ -394,14 +398,16 @@ def run_ours(a):
     if rank == 0:
         peaks, peak_src = measured_peaks()
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        achieved = attn_flops_per_launch / (attn_avg_ms * 1e-3) / 1e12
+        achieved = attn_flops_per_launch / (attn_avg_ms * 1e-3) / 1e12 if attn_avg_ms > 0 else 0.0
         line = {
             "metric": METRIC, "value": total_flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (SplitMix64 uniform[-1,1) -> bf16, seed {a.seed}, generated on "
                     "device per rank shard)",
-            "config": workload_config(a, world),
+            "config": dict(workload_config(a, world), transport=a.transport,
+                           **({"test_mode": "all ranks share cuda:0 (TR_BENCH_SHARED_DEVICE)"}
+                              if shared else {})),
             "tokens_per_s": S / (ms * 1e-3),
             "exposed_comm_ms_per_step": exposed,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,

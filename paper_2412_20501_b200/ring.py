@@ -239,14 +239,23 @@ class TokenRingAttention:
             self.ops.init_(self.acc_out, self.acc_lse)
         local_layout = self.prog[0].q_layout
         ev_comp, ev_out_sent = {}, {}
+        self.timeline = []
         for st in self.prog:
             i = st.step
+            ev = {}
+            if self.record_timeline:
+                ev["start"] = self.ops.event()
+                self.ops.record(ev["start"])
             if i >= 1 and (st.q_ids or st.send_q):
                 for src, _ in self.prog[i - 1].recv_q:                  # Q_i has landed
                     kernels.flag_wait_(self.flags[4 + src:5 + src], base + i, cur)
             if i >= 1 and self.prog[i - 1].recv_out:
-                # OUT sent to me at step i-1 has landed: merge it, free the buffer
                 kernels.flag_wait_(self.flags[2:3], base + i - 1, cur)
+            if self.record_timeline:
+                ev["comm_ready"] = self.ops.event()
+                self.ops.record(ev["comm_ready"])
+            if i >= 1 and self.prog[i - 1].recv_out:
+                # OUT sent to me at step i-1 has landed: merge it, free the buffer
                 src, ids = self.prog[i - 1].recv_out[0]
                 n = len(ids) * c
                 self._merge_returned((ids, self.out_recv[:n],
@@ -287,12 +296,19 @@ class TokenRingAttention:
                 kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
                             self.sched.chunks[b].start) for b in st.kv_ids]
                 buf = i % 2
+                if self.record_timeline:
+                    ev["attn_start"] = self.ops.event()
+                    self.ops.record(ev["attn_start"])
                 if i == 0 and self.direct_first:
                     self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
                                        self.acc_out, self.acc_lse)
                 else:
                     self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
                                        self.obuf[buf], self.lbuf[buf])
+                if self.record_timeline:
+                    ev["attn_end"] = self.ops.event()
+                    self.ops.record(ev["attn_end"])
+                    ev["attn_flops"] = self.step_flops(st)
                 if st.accumulate and not (i == 0 and self.direct_first):
                     for a in st.q_ids:
                         r0, r1 = _rows(st.q_layout, (a,), c)
@@ -301,6 +317,10 @@ class TokenRingAttention:
                                         self.obuf[buf][r0:r1], self.lbuf[buf][:, r0:r1])
             ev_comp[i] = torch.cuda.Event()
             ev_comp[i].record(cur)
+            if self.record_timeline:
+                ev["computed"] = self.ops.event()
+                self.ops.record(ev["computed"])
+                self.timeline.append(ev)
             if i < P:
                 # my traveling-Q slot i%2 is free once both this step's compute
                 # and my own forward copy of it are done
