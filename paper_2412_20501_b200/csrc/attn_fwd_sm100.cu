@@ -435,6 +435,394 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   }
 }
 
+#ifdef TR_KERNEL_PAIR
+// Opt-in build variant (python -m paper_2412_20501_b200.build -D TR_KERNEL_PAIR):
+// parity-green, faster in short bursts, slower than attn_fwd_sm100_kernel under
+// the 1000 W power cap.  Not compiled into the product library.
+// exp2 of 64 scores -> 32 packed bf16x2 words of P; row-sum in lsum2.
+template <int POLY_MOD, bool kPoly>
+__device__ __forceinline__ void p_row64(const uint32_t (&s)[64], uint64_t c2, uint64_t nmc2,
+                                        uint64_t (&lsum2)[2], uint32_t (&pk)[32]) {
+  #pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint64_t x2 =
+        ffma2(f2pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nmc2);
+    float a, b;
+    f2unpack(x2, a, b);
+    uint64_t p2;
+    if (kPoly && (i % POLY_MOD) == POLY_MOD - 1)
+      p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f)));
+    else
+      p2 = f2pack(ex2_approx(a), ex2_approx(b));
+    lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
+    float pa, pb;
+    f2unpack(p2, pa, pb);
+    pk[i] = pack_bf16x2(pa, pb);
+  }
+}
+
+// ============================================================================
+// attn_fwd_pair: the D=128 kernel.  A CTA PAIR (cluster of 2 on one TPC)
+// computes one head x 256 query rows with cta_group::2 MMAs (M=256): CTA r
+// holds q rows [128r, 128r+128) and HALF of every K tile (keys 64r..64r+63)
+// and V tile (head-dim columns 64r..64r+63), so each SM streams the same
+// K/V bytes per flop as a 256-row CTA while its TMEM holds only one 128-row
+// tile -- room for DOUBLE-BUFFERED S:
+//   TMEM (512 cols, same columns in both CTAs): S_buf at buf*128,
+//   O_A at 256, O_B at 384.
+// The softmax of each CTA is split by KEY COLUMNS over its 8 warps into two
+// independent online softmaxes (group g owns keys 64g..64g+63 of every tile
+// and accumulates O_g); the two are merged row by row in the epilogue.
+// Leader (rank 0) MMA order:  S(0) S(1) | per j: O_A+=P_A(j)V_j[keys 0:64]
+//                                               O_B+=P_B(j)V_j[keys 64:128]
+//                                               S(j+2) -> buffer j&1
+// so S(j+1) is in TMEM while softmax(j) runs: the P -> P.V -> next-S chain is
+// off the critical path.  K/V halves cross each CTA's ring in consumption
+// order K0 K1 V0 K2 V1 ...; TMA completions count on the leader's barriers,
+// MMA completions are multicast to both CTAs, P hand-offs arrive (one per
+// warp) on the leader's barriers.
+struct PairCfg {
+  static constexpr int D = 128;
+  static constexpr int QBOX = 128 * 64 * 2;       // q tile box: 128 rows x 64 cols
+  static constexpr int QTILE = 2 * QBOX;          // this CTA's 128 q rows (32 KB)
+  static constexpr int KBOX = 64 * 64 * 2;        // K half box: 64 keys x 64 cols
+  static constexpr int STAGE = 16384;             // K half (2 x KBOX) or V half (128 x 64)
+  static constexpr int NS = 12;                   // ring stages
+  static constexpr int THREADS = 384;
+  static constexpr int SMEM_TILES = QTILE + NS * STAGE;
+  static constexpr int SMEM = SMEM_TILES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+  static constexpr uint32_t IDESC_QK = idesc_bf16(256, 128, false);
+  static constexpr uint32_t IDESC_PV = idesc_bf16(256, 128, true);
+  static constexpr float RESCALE_LOG2 = 8.0f;
+  static constexpr int POLY_MOD = TR_POLY_MOD;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk64,
+                     const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnPlan p) {
+  using C = PairCfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + C::QTILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_TILES);
+  uint64_t* q_full = bars + 0;               // leader: both q halves landed
+  uint64_t* kv_full = bars + 1;              // [NS] leader: both halves of a stage landed
+  uint64_t* kv_empty = kv_full + C::NS;      // [NS] both CTAs (multicast commit)
+  uint64_t* s_full = kv_empty + C::NS;       // [2 buffers] both CTAs
+  uint64_t* p_full = s_full + 2;             // [2 buffers][2 groups] leader, 8 warp arrivals
+  uint64_t* pv_done = p_full + 4;            // [2 groups] both CTAs
+  uint64_t* o_done = pv_done + 2;            // [1] both CTAs
+  int64_t* kv_tiles = reinterpret_cast<int64_t*>(o_done + 1);   // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 5);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t pair = blockIdx.x >> 1;
+  const int head = static_cast<int>(pair / p.tile_prefix[p.nq]);
+  const int64_t lin = pair % p.tile_prefix[p.nq];
+  int qseg;
+  int64_t qrow0;                             // first row of the pair's 256-row tile
+  q_tile_of(p, lin, qseg, qrow0);
+  const tr_segment Q = p.q[qseg];
+  const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
+  const int64_t my_row0 = qrow0 + 128 * rank;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int b = 0; b < 2; ++b) mbar_init(&s_full[b], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 8);
+    for (int g = 0; g < 2; ++g) mbar_init(&pv_done[g], 1);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmq); tma_prefetch_desc(&tmk64); tma_prefetch_desc(&tmv);
+  }
+  if (warp == 2 && lane < TR_MAX_SEGMENTS) {
+    int64_t n = 0;
+    if (lane < p.nkv) {
+      n = (p.kv[lane].rows + 127) / 128;
+      if (p.causal)
+        n = (qmax_pos < p.kv[lane].pos0) ? 0 : imin64(n, (qmax_pos - p.kv[lane].pos0) / 128 + 1);
+    }
+    kv_tiles[lane] = n;
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                            // peer barriers initialised before any remote use
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const int ntiles = __shfl_sync(
+      0xffffffffu, static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]), 0);
+
+  if (warp < 4) {
+   setmaxnreg_dec<56>();
+   if (warp == 0 && ntiles > 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    const int32_t col0 = head * D;
+    const uint32_t lq_full = mapa_u32(smem_u32(q_full), 0);
+    if (rank == 0) mbar_arrive_expect_tx_elect(q_full, 2 * C::QTILE);
+    for (int b = 0; b < 2; ++b)
+      tma_load_2d_pair_elect(sQ + b * C::QBOX, &tmq, lq_full, col0 + 64 * b,
+                             static_cast<int32_t>(Q.row0 + my_row0), kEvictFirst);
+    int s = 0;
+    uint32_t round = 0;
+    auto put = [&](bool is_v, int64_t krow) {
+      mbar_wait_cluster(&kv_empty[s], (round & 1) ^ 1);
+      if (rank == 0) mbar_arrive_expect_tx_elect(&kv_full[s], 2 * C::STAGE);
+      const uint32_t lbar = mapa_u32(smem_u32(&kv_full[s]), 0);
+      uint8_t* dst = sKV + s * C::STAGE;
+      if (is_v) {          // V half: keys krow..+127, head-dim columns 64*rank..+63
+        tma_load_2d_pair_elect(dst, &tmv, lbar, col0 + 64 * static_cast<int32_t>(rank),
+                               static_cast<int32_t>(krow), kEvictLast);
+      } else {             // K half: keys krow+64*rank..+63, all 128 head-dim columns
+        for (int b = 0; b < 2; ++b)
+          tma_load_2d_pair_elect(dst + b * C::KBOX, &tmk64, lbar, col0 + 64 * b,
+                                 static_cast<int32_t>(krow + 64 * rank), kEvictLast);
+      }
+      if (++s == C::NS) { s = 0; ++round; }
+    };
+    KvWalk wk = kv_begin(kv_tiles), wv = wk;
+    put(false, p.kv[wk.g].row0 + wk.t * 128);                        // K_0
+    wk.next(kv_tiles);
+    for (int j = 0; j < ntiles; ++j) {
+      if (j + 1 < ntiles) {                                           // K_{j+1}
+        put(false, p.kv[wk.g].row0 + wk.t * 128);
+        wk.next(kv_tiles);
+      }
+      put(true, p.kv[wv.g].row0 + wv.t * 128);                        // V_j
+      wv.next(kv_tiles);
+    }
+   } else if (warp == 1 && rank == 0 && ntiles > 0) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint64_t dQ = sdesc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t dK = sdesc_sw128(smem_u32(sKV), 16, 1024);       // K-major
+    const uint64_t dV = sdesc_sw128(smem_u32(sKV), C::STAGE, 1024); // MN-major, 64 cols / CTA
+    int s = 0;
+    uint32_t round = 0;
+    auto take = [&]() {
+      mbar_wait(&kv_full[s], round & 1);
+      tc_fence_after();
+      const int slot = s;
+      if (++s == C::NS) { s = 0; ++round; }
+      return slot;
+    };
+    auto qk = [&](int buf, int slot) {
+      const uint64_t b0 = dK + static_cast<uint32_t>((slot * C::STAGE) >> 4);
+      #pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t oa = ((kk / 4) * C::QBOX + (kk % 4) * 32) >> 4;
+        const uint32_t ob = ((kk / 4) * C::KBOX + (kk % 4) * 32) >> 4;
+        mma2_ss_elect(tmem + buf * 128, desc_add(dQ, oa), desc_add(b0, ob), C::IDESC_QK, kk > 0);
+      }
+    };
+    auto pv = [&](int buf, int g, int slot, bool acc) {
+      const uint64_t b0 = dV + static_cast<uint32_t>((slot * C::STAGE) >> 4);
+      #pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4)
+        mma2_ts_elect(tmem + 256 + g * 128, tmem + buf * 128 + 64 * g + 8 * k4,
+                      desc_add(b0, ((g * 4 + k4) * 2048) >> 4), C::IDESC_PV,
+                      (acc || k4 > 0) ? 1u : 0u);
+    };
+    for (int j = 0; j < 2 && j < ntiles; ++j) {
+      const int slot = take();
+      qk(j, slot);
+      tc_commit2_elect(&s_full[j]);
+      tc_commit2_elect(&kv_empty[slot]);
+    }
+    for (int j = 0; j < ntiles; ++j) {
+      const int buf = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      TR_TRACE_AT(0, j);
+      const int vslot = take();
+      mbar_wait_cluster(&p_full[buf * 2 + 0], ph);
+      tc_fence_after();
+      TR_TRACE_AT(1, j);
+      pv(buf, 0, vslot, j > 0);
+      tc_commit2_elect(&pv_done[0]);
+      mbar_wait_cluster(&p_full[buf * 2 + 1], ph);
+      tc_fence_after();
+      TR_TRACE_AT(2, j);
+      pv(buf, 1, vslot, j > 0);
+      tc_commit2_elect(&pv_done[1]);
+      tc_commit2_elect(&kv_empty[vslot]);
+      if (j == ntiles - 1) tc_commit2_elect(o_done);
+      if (j + 2 < ntiles) {
+        const int kslot = take();
+        qk(buf, kslot);
+        tc_commit2_elect(&s_full[buf]);
+        tc_commit2_elect(&kv_empty[kslot]);
+      }
+      TR_TRACE_AT(3, j);
+    }
+   }
+  } else {
+   setmaxnreg_inc<224>();
+   {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int g = (warp - 4) / 4;            // key group: columns [64g, 64g+64)
+    const int quarter = warp % 4;            // TMEM lane quarter
+    const int r = quarter * 32 + lane;       // row inside this CTA's 128 rows
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + 64 * g;       // + buf * 128
+    const uint32_t tOg = tmem + lane_base + 256 + g * 128;
+    const int64_t row_in_seg = my_row0 + r;
+    const int64_t my_pos = Q.pos0 + row_in_seg;
+    const int64_t tile_min_pos = Q.pos0 + my_row0;
+    const float c = p.scale_log2;
+    const float thresh = C::RESCALE_LOG2 / c;
+    const uint64_t c2 = f2pack(c, c);
+    const uint32_t pbar0 = mapa_u32(smem_u32(p_full), 0);   // leader's p_full[0]
+    float m_used = -INFINITY;
+    uint64_t lsum2[2] = {0ull, 0ull};
+    KvWalk w = kv_begin(kv_tiles);
+    for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
+      const int buf = j & 1;
+      const int64_t kpos = p.kv[w.g].pos0 + w.t * 128 + 64 * g;
+      const int64_t left = p.kv[w.g].rows - w.t * 128 - 64 * g;
+      const int valid = static_cast<int>(imax64(0, imin64(64, left)));
+      TR_TRACE_AT(0, j);
+      mbar_wait(&s_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      TR_TRACE_AT(1, j);
+      uint32_t s[64];
+      tmem_ld32_at<0>(tS + buf * 128, s);
+      tmem_ld32_at<32>(tS + buf * 128 + 32, s);
+      tc_wait_ld();
+      const bool need_mask = valid < 64 || (p.causal && kpos + 63 > tile_min_pos);
+      if (need_mask) {
+        int64_t lim = valid;
+        if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
+        const int limit = static_cast<int>(imax64(lim, 0));
+        #pragma unroll
+        for (int i = 0; i < 64; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;  // -inf
+      }
+      float m4[4];
+      #pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        float m = __uint_as_float(s[16 * a]);
+        #pragma unroll
+        for (int i = 16 * a + 1; i < 16 * a + 15; i += 2)
+          m = fmaxf(m, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
+        m4[a] = fmaxf(m, __uint_as_float(s[16 * a + 15]));
+      }
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      TR_TRACE_AT(2, j);
+      const bool grow = mx > m_used + thresh;
+      const bool scale_o = grow && m_used != -INFINITY;
+      if (__any_sync(0xffffffffu, scale_o)) {
+        // O_g may still be accumulating P_g(j-1).V_{j-1}: wait for it
+        mbar_wait(&pv_done[g], (j - 1) & 1);
+        tc_fence_after();
+        const float f = scale_o ? ex2_approx((m_used - mx) * c) : 1.f;
+        const uint64_t f2 = f2pack(f, f);
+        lsum2[0] = fmul2(lsum2[0], f2);
+        lsum2[1] = fmul2(lsum2[1], f2);
+        #pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t u[32];
+          tmem_ld32(tOg + cc * 32, u);
+          tc_wait_ld();
+          #pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t v = fmul2(f2pack(__uint_as_float(u[i]), __uint_as_float(u[i + 1])), f2);
+            u[i] = static_cast<uint32_t>(v);
+            u[i + 1] = static_cast<uint32_t>(v >> 32);
+          }
+          tmem_st32(tOg + cc * 32, u);
+        }
+      }
+      if (grow) m_used = mx;
+      const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
+      const uint64_t nmc2 = f2pack(-mc, -mc);
+      uint32_t pk[32];
+      if (need_mask) p_row64<C::POLY_MOD, false>(s, c2, nmc2, lsum2, pk);
+      else p_row64<C::POLY_MOD, true>(s, c2, nmc2, lsum2, pk);
+      tmem_st32(tS + buf * 128, pk);
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(pbar0 + 8u * (buf * 2 + g));
+      TR_TRACE_AT(3, j);
+    }
+    float l;
+    {
+      float a0, a1, b0, b1;
+      f2unpack(lsum2[0], a0, a1);
+      f2unpack(lsum2[1], b0, b1);
+      l = (a0 + a1) + (b0 + b1);
+    }
+    // ---------------------------------------------------------- epilogue
+    if (ntiles > 0) {
+      mbar_wait(o_done, 0);
+      tc_fence_after();
+    }
+    float2* red = reinterpret_cast<float2*>(sQ);    // q tile is free once o_done fired
+    red[g * 128 + r] = make_float2(m_used, l);
+    named_barrier_sync(1, 256);
+    const float2 other = red[(1 - g) * 128 + r];
+    const float m = fmaxf(m_used, other.x);
+    const float f_me = (m_used == -INFINITY) ? 0.f : ex2_approx((m_used - m) * c);
+    const float f_ot = (other.x == -INFINITY) ? 0.f : ex2_approx((other.x - m) * c);
+    const float L = l * f_me + other.y * f_ot;
+    const float inv = (L > 0.f) ? 1.f / L : 0.f;
+    const float fa = (g == 0 ? f_me : f_ot) * inv;
+    const float fb = (g == 0 ? f_ot : f_me) * inv;
+    const bool row_ok = row_in_seg < Q.rows;
+    const int64_t grow_ = Q.row0 + row_in_seg;
+    const int64_t oidx = (grow_ * p.heads + head) * D;
+    const uint32_t tOA = tmem + lane_base + 256;
+    const uint32_t tOB = tOA + 128;
+    #pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int col = g * 64 + cc * 32;
+      uint32_t ua[32], ub[32];
+      if (ntiles > 0) {
+        tmem_ld32(tOA + col, ua);
+        tmem_ld32(tOB + col, ub);
+        tc_wait_ld();
+      } else {
+        #pragma unroll
+        for (int i = 0; i < 32; ++i) { ua[i] = 0u; ub[i] = 0u; }
+      }
+      float o[32];
+      #pragma unroll
+      for (int i = 0; i < 32; ++i)
+        o[i] = __uint_as_float(ua[i]) * fa + __uint_as_float(ub[i]) * fb;
+      if (!row_ok) continue;
+      if (p.out_f32) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oidx + col);
+        #pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+      } else {
+        uint32_t pk[16];
+        #pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(o[2 * i], o[2 * i + 1]);
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oidx + col);
+        #pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+    if (row_ok && g == 0)
+      p.lse[head * p.lse_stride + grow_] = (L > 0.f) ? (logf(L) + m * p.scale) : -INFINITY;
+   }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                            // the leader's MMAs read this CTA's smem/TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, 512);
+  }
+}
+
+#endif  // TR_KERNEL_PAIR
+
 #ifdef TR_TRACE
 extern "C" int tr_debug_trace(void* dst, size_t bytes) {
   return cudaMemcpyFromSymbol(dst, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace)) ==
@@ -461,12 +849,13 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-static int make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t row_elems) {
+static int make_tmap(CUtensorMap* map, const void* base, int64_t rows, int64_t row_elems,
+                     uint32_t box_rows = 128) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(TR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_elems), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_elems * 2)};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -509,9 +898,38 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
   return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
 }
 
+#ifdef TR_KERNEL_PAIR
+static int launch_pair(const void* q, const void* k, const void* v, int64_t tq_total,
+                       int64_t tk_total, AttnPlan& plan, cudaStream_t s) {
+  using C = PairCfg;
+  CUtensorMap tq, tk, tv;
+  const int64_t row_elems = int64_t(plan.heads) * C::D;
+  int rc;
+  if ((rc = make_tmap(&tq, q, tq_total, row_elems, 128))) return rc;
+  if ((rc = make_tmap(&tk, k, tk_total, row_elems, 64))) return rc;
+  if ((rc = make_tmap(&tv, v, tk_total, row_elems, 128))) return rc;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_pair_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_pair)");
+    attr_done = true;
+  }
+  const int64_t pairs = plan.tile_prefix[plan.nq] * plan.heads;
+  if (pairs == 0) return TR_OK;
+  if (2 * pairs > 0x7FFFFFFF) return fail(TR_ERR_UNSUPPORTED, "grid too large");
+  attn_fwd_pair_kernel<<<static_cast<unsigned>(2 * pairs), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
+  return cuda_status(cudaGetLastError(), "attn_fwd_pair launch");
+}
+#endif  // TR_KERNEL_PAIR
+
 int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_total,
                       int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s) {
+#ifdef TR_KERNEL_PAIR
+  if (head_dim == 128) return launch_pair(q, k, v, tq_total, tk_total, plan, s);
+#else
   if (head_dim == 128) return launch_d<128>(q, k, v, tq_total, tk_total, plan, s);
+#endif
   if (head_dim == 64) return launch_d<64>(q, k, v, tq_total, tk_total, plan, s);
   return fail(TR_ERR_UNSUPPORTED, "sm100 attention kernel supports head_dim 64 or 128");
 }
