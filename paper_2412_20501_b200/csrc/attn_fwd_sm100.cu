@@ -56,14 +56,24 @@ struct AttnCfg {
 #ifdef TR_TRACE
 // Debug-only timeline of CTA 0 (clock64 per role and kv tile); read back with
 // tr_debug_trace().  Not compiled into the product library.
-__device__ unsigned long long g_trace[12 * 64 * 8];
+// CTAs 0 and 1 (a pair in the TR_KERNEL_PAIR build); slots 0-5 clock64,
+// slot 6-7 free; TR_TRACE_GT(slot) records %globaltimer (cross-SM).
+__device__ unsigned long long g_trace[2 * 12 * 64 * 8];
 #define TR_TRACE_AT(slot, jj)                                                        \
   do {                                                                               \
-    if (blockIdx.x == 0 && lane == 0 && (jj) < 64)                                   \
-      g_trace[(warp * 64 + (jj)) * 8 + (slot)] = clock64();                          \
+    if (blockIdx.x < 2 && lane == 0 && (jj) < 64)                                    \
+      g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = clock64();      \
+  } while (0)
+#define TR_TRACE_GT(slot, jj)                                                        \
+  do {                                                                               \
+    if (blockIdx.x < 2 && lane == 0 && (jj) < 64)                                    \
+      g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = globaltimer_ns(); \
   } while (0)
 #else
 #define TR_TRACE_AT(slot, jj) \
+  do {                        \
+  } while (0)
+#define TR_TRACE_GT(slot, jj) \
   do {                        \
   } while (0)
 #endif
@@ -502,6 +512,11 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
                      const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnPlan p) {
   using C = PairCfg;
   constexpr int D = C::D;
+#ifndef TR_PAIR_MMA_WARP
+#define TR_PAIR_MMA_WARP 1
+#define TR_PAIR_PROD_WARP 0
+#endif
+  constexpr int kMmaWarp = TR_PAIR_MMA_WARP, kProdWarp = TR_PAIR_PROD_WARP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -549,7 +564,7 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
     }
     kv_tiles[lane] = n;
   }
-  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc2(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   cluster_sync();                            // peer barriers initialised before any remote use
@@ -560,7 +575,7 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
 
   if (warp < 4) {
    setmaxnreg_dec<56>();
-   if (warp == 0 && ntiles > 0) {
+   if (warp == kProdWarp && ntiles > 0) {
     // ------------------------------------------------------------ producer (both CTAs)
     const int32_t col0 = head * D;
     const uint32_t lq_full = mapa_u32(smem_u32(q_full), 0);
@@ -596,7 +611,7 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
       put(true, p.kv[wv.g].row0 + wv.t * 128);                        // V_j
       wv.next(kv_tiles);
     }
-   } else if (warp == 1 && rank == 0 && ntiles > 0) {
+   } else if (warp == kMmaWarp && rank == 0 && ntiles > 0) {
     // ------------------------------------------------------------ MMA issuer (leader)
     mbar_wait(q_full, 0);
     tc_fence_after();
@@ -640,9 +655,11 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
       const uint32_t ph = (j >> 1) & 1;
       TR_TRACE_AT(0, j);
       const int vslot = take();
+      TR_TRACE_AT(4, j);
       mbar_wait_cluster(&p_full[buf * 2 + 0], ph);
       tc_fence_after();
       TR_TRACE_AT(1, j);
+      TR_TRACE_GT(5, j);
       pv(buf, 0, vslot, j > 0);
       tc_commit2_elect(&pv_done[0]);
       mbar_wait_cluster(&p_full[buf * 2 + 1], ph);
@@ -747,6 +764,7 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
+      TR_TRACE_GT(5, j);
       if (lane == 0) mbar_arrive_cluster(pbar0 + 8u * (buf * 2 + g));
       TR_TRACE_AT(3, j);
     }
@@ -815,7 +833,7 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
   tc_fence_before();
   __syncthreads();
   cluster_sync();                            // the leader's MMAs read this CTA's smem/TMEM
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc2(tmem, 512);
   }
