@@ -491,6 +491,11 @@ __device__ __forceinline__ void p_row64(const uint32_t (&s)[64], uint64_t c2, ui
 // order K0 K1 V0 K2 V1 ...; TMA completions count on the leader's barriers,
 // MMA completions are multicast to both CTAs, P hand-offs arrive (one per
 // warp) on the leader's barriers.
+#ifdef TR_PAIR_SLEEP_NS
+#define PAIR_WAIT(bar, par) mbar_wait_backoff(bar, par, TR_PAIR_SLEEP_NS)
+#else
+#define PAIR_WAIT(bar, par) mbar_wait_cluster(bar, par)
+#endif
 struct PairCfg {
   static constexpr int D = 128;
   static constexpr int QBOX = 128 * 64 * 2;       // q tile box: 128 rows x 64 cols
@@ -586,7 +591,7 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
     int s = 0;
     uint32_t round = 0;
     auto put = [&](bool is_v, int64_t krow) {
-      mbar_wait_cluster(&kv_empty[s], (round & 1) ^ 1);
+      PAIR_WAIT(&kv_empty[s], (round & 1) ^ 1);
       if (rank == 0) mbar_arrive_expect_tx_elect(&kv_full[s], 2 * C::STAGE);
       const uint32_t lbar = mapa_u32(smem_u32(&kv_full[s]), 0);
       uint8_t* dst = sKV + s * C::STAGE;
@@ -656,13 +661,13 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
       TR_TRACE_AT(0, j);
       const int vslot = take();
       TR_TRACE_AT(4, j);
-      mbar_wait_cluster(&p_full[buf * 2 + 0], ph);
+      PAIR_WAIT(&p_full[buf * 2 + 0], ph);
       tc_fence_after();
       TR_TRACE_AT(1, j);
       TR_TRACE_GT(5, j);
       pv(buf, 0, vslot, j > 0);
       tc_commit2_elect(&pv_done[0]);
-      mbar_wait_cluster(&p_full[buf * 2 + 1], ph);
+      PAIR_WAIT(&p_full[buf * 2 + 1], ph);
       tc_fence_after();
       TR_TRACE_AT(2, j);
       pv(buf, 1, vslot, j > 0);

@@ -73,6 +73,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Wait with nanosleep back-off between polls, for a warp that shares its
+// SM sub-partition with softmax warps: a tight try_wait loop steals their
+// issue slots.  `ns` trades observation latency for issue slots.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  for (uint32_t it = 1;; ++it) {
+    __nanosleep(ns);
+    if (mbar_try_wait(addr, parity)) return;
+    if ((it & 255u) == 0 && globaltimer_ns() - t0 > 20000000000ull) __trap();
+  }
+}
+
 // named barrier among `nthreads` threads (id 0 is __syncthreads)
 __device__ __forceinline__ void named_barrier_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

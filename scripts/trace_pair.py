@@ -23,7 +23,8 @@ L.tr_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert L.tr_debug_trace(buf.ctypes.data, buf.nbytes) == 0
 t = buf.reshape(2, 12, 64, 8).astype(np.int64)
 J = slice(8, 60)
-mma = t[0, 1]
+MW = int(os.environ.get("MMA_WARP", 1))
+mma = t[0, MW]
 print("MMA (leader, clock64): iter start -> V landed", np.median(mma[J, 4] - mma[J, 0]),
       " V -> P_A seen", np.median(mma[J, 1] - mma[J, 4]), " P_A -> P_B", np.median(mma[J, 2] - mma[J, 1]),
       " P_B -> end", np.median(mma[J, 3] - mma[J, 2]), " period", np.median(np.diff(mma[8:60, 0])))
@@ -34,8 +35,14 @@ for cta in (0, 1):
               f"{np.median(s[J, 2] - s[J, 1]):.0f} max->P done {np.median(s[J, 3] - s[J, 2]):.0f} "
               f"P done->next S ready {np.median(s[9:61, 1] - s[J, 3]):.0f}")
 # globaltimer (ns): softmax P published (slot 5) in both CTAs vs MMA P_A seen (slot 5)
-seen = t[0, 1][J, 5]
+seen = t[0, MW][J, 5]
 for cta in (0, 1):
     for w in (4, 5, 6, 7, 8, 9, 10, 11):
         pub = t[cta, w][J, 5]
         print(f"  cta {cta} warp {w:2d}: MMA sees P_A  {np.median(seen - pub):7.0f} ns after this warp published")
+print("leader CTA, per warp (clock64, relative to warp 4): S ready, max done, P done")
+base = t[0, 4][J]
+for w in range(4, 12):
+    s = t[0, w][J]
+    print(f"  warp {w:2d}: {np.median(s[:, 1] - base[:, 1]):6.0f} {np.median(s[:, 2] - base[:, 2]):6.0f} "
+          f"{np.median(s[:, 3] - base[:, 3]):6.0f}")
