@@ -49,8 +49,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
-                    help="N>1 exchange: NCCL P2P (default) or copy-engine CUDA IPC")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc", "fused"],
+                    help="N>1 exchange: NCCL P2P (default), copy-engine CUDA IPC, or fused "
+                         "(IPC for Q, OUT rows stored by the attention epilogue into the "
+                         "home rank's buffer)")
     return ap.parse_args()
 
 
@@ -308,8 +310,8 @@ def run_ours(a):
     # box -- every rank on cuda:0, copy-engine transport, gloo for the host
     # collectives.  Numbers from it are not scaling numbers.
     shared = os.environ.get("TR_BENCH_SHARED_DEVICE") == "1" and world > 1
-    if shared and a.transport != "ipc":
-        raise SystemExit("TR_BENCH_SHARED_DEVICE=1 needs --transport ipc")
+    if shared and a.transport not in ("ipc", "fused"):
+        raise SystemExit("TR_BENCH_SHARED_DEVICE=1 needs --transport ipc or fused")
     dev_index = 0 if shared else local
     torch.cuda.set_device(dev_index)
     if world > 1:
@@ -371,6 +373,8 @@ def run_ours(a):
     for tl in timelines:
         for ev in tl:
             stall += ev["start"].elapsed_time(ev["comm_ready"])
+            if "grant_wait" in ev:             # fused: wait for the home's slot grant
+                stall += ev["grant_wait"].elapsed_time(ev["granted"])
             if "attn_start" in ev:
                 kern_ms += ev["attn_start"].elapsed_time(ev["attn_end"])
                 kern_flops += ev["attn_flops"]

@@ -81,6 +81,24 @@ int tr_attention_segments(const void* q, const void* k, const void* v, void* out
                           const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
                           int32_t n_kv, int32_t causal, int32_t out_dtype, void* stream);
 
+/* tr_attention_segments fused with the OUT_LSE message of the next step
+ * (engine.py:346-353 sends the rows computed at step i to their home at step
+ * i+1, where MergePlan folds them in, engine.py:187-200): the epilogue stores
+ * the bf16 rows and their lse straight into the HOME rank's receive buffer --
+ * `out`/`lse` may be CUDA-IPC-mapped peer memory, so the transfer rides
+ * NVLink/NVSwitch tile by tile while the rest of the grid still computes.
+ * Row r of q's local buffer lands at row r - row_shift of out (and of each
+ * lse head row, stride lse_stride).  If done_flag != NULL the last CTA to
+ * finish raises *done_flag to done_value with a system-scope release (after
+ * every CTA's stores are fenced); done_count is a zeroed device counter the
+ * launch uses and leaves zeroed. */
+int tr_attention_segments_push(const void* q, const void* k, const void* v, void* out, float* lse,
+                               int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
+                               const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
+                               int32_t n_kv, int32_t causal, int64_t row_shift, int64_t lse_stride,
+                               uint32_t* done_count, uint64_t* done_flag, uint64_t done_value,
+                               void* stream);
+
 /* kernels.merge_state, in place on a float32 accumulator:
  *   acc <- merge(acc, blk)     (ref _kernels.pyx:68-102)
  * blk_out is bf16 or f32 (blk_dtype); -inf rows are exact identities.

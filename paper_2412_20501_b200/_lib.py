@@ -26,7 +26,8 @@ TR_DTYPE_F32 = 0
 TR_DTYPE_BF16 = 1
 
 # every symbol include/tokenring.h declares
-EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_merge_state", "tr_partial_init",
+EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
+           "tr_merge_state", "tr_partial_init",
            "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_copy_async", "tr_version",
            "tr_kernel_count", "tr_last_error")
 
@@ -54,6 +55,10 @@ def _declare(lib):
     lib.tr_attention_segments.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32,
                                           ctypes.POINTER(Segment), i32,
                                           ctypes.POINTER(Segment), i32, i32, i32, vp]
+    lib.tr_attention_segments_push.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32,
+                                               ctypes.POINTER(Segment), i32,
+                                               ctypes.POINTER(Segment), i32, i32, i64, i64,
+                                               vp, vp, ctypes.c_uint64, vp]
     lib.tr_merge_state.argtypes = [vp, vp, vp, i32, vp, i64, i32, i32, i64, i64, vp, vp]
     lib.tr_partial_init.argtypes = [vp, vp, i64, i32, i32, vp]
     lib.tr_splitmix_bf16.argtypes = [ctypes.c_uint64, i64, i64, ctypes.c_double,
@@ -61,7 +66,8 @@ def _declare(lib):
     lib.tr_flag_set.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tr_flag_wait.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tr_copy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
-    for name in ("tr_attention_block", "tr_attention_segments", "tr_merge_state",
+    for name in ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
+                 "tr_merge_state",
                  "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
                  "tr_copy_async"):
         getattr(lib, name).restype = ctypes.c_int

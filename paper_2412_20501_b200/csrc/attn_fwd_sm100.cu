@@ -438,11 +438,13 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
    }
   }
   tc_fence_before();
+  if (p.done_flag) __threadfence_system();   // out/lse rows may live on a peer GPU
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (p.done_flag && threadIdx.x == 0) signal_done(p);
 }
 
 #ifdef TR_KERNEL_PAIR
@@ -836,12 +838,14 @@ attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_const
    }
   }
   tc_fence_before();
+  if (p.done_flag) __threadfence_system();
   __syncthreads();
   cluster_sync();                            // the leader's MMAs read this CTA's smem/TMEM
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc2(tmem, 512);
   }
+  if (p.done_flag && threadIdx.x == 0) signal_done(p);
 }
 
 #endif  // TR_KERNEL_PAIR

@@ -42,10 +42,19 @@ static int check_segments(const tr_segment* segs, int n, int64_t total, const ch
   return TR_OK;
 }
 
+// Push options of tr_attention_segments_push (all zero for a local launch).
+struct PushOpts {
+  int64_t row_shift = 0;           // out/lse row r lands at row r - row_shift
+  int64_t lse_stride = -1;         // row stride of lse (-1: tq_total)
+  unsigned int* done_count = nullptr;
+  unsigned long long* done_flag = nullptr;
+  unsigned long long done_value = 0;
+};
+
 static int run_segments(const void* q, const void* k, const void* v, void* out, float* lse,
                         int64_t tq_total, int64_t tk_total, int heads, int head_dim,
                         const tr_segment* qs, int nq, const tr_segment* ks, int nk, int causal,
-                        int out_dtype, cudaStream_t s) {
+                        int out_dtype, cudaStream_t s, const PushOpts& push = PushOpts()) {
   if (out_dtype != TR_DTYPE_BF16 && out_dtype != TR_DTYPE_F32)
     return fail(TR_ERR_CONFIG, "out_dtype must be TR_DTYPE_BF16 or TR_DTYPE_F32");
   if (heads < 1 || head_dim < 1 || tq_total < 0 || tk_total < 0)
@@ -60,21 +69,39 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   plan.nkv = 0;
   for (int i = 0; i < nk; ++i)
     if (ks[i].rows > 0) plan.kv[plan.nkv++] = ks[i];
-  if (plan.nq == 0) return TR_OK;
+  // a pushing launch with nothing to compute still owes its receiver the flag
+  auto flag_only = [&]() {
+    return push.done_flag ? launch_flag_set(push.done_flag, push.done_value, s) : TR_OK;
+  };
+  if (plan.nq == 0) return flag_only();
   plan.causal = causal ? 1 : 0;
   plan.heads = heads;
-  plan.lse_stride = tq_total;
+  plan.lse_stride = push.lse_stride >= 0 ? push.lse_stride : tq_total;
   plan.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(head_dim)));
   plan.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(head_dim)));
-  plan.out = out;
   plan.out_f32 = out_dtype == TR_DTYPE_F32 ? 1 : 0;
-  plan.lse = lse;
+  // shifted bases: the kernels index rows of q's local buffer; row r of out /
+  // lse is written at r - row_shift (a receive buffer holding only the rows
+  // of one message).  Only rows >= row_shift are ever written.
+  const int64_t esz = plan.out_f32 ? 4 : 2;
+  plan.out = reinterpret_cast<void*>(reinterpret_cast<uintptr_t>(out) -
+                                     static_cast<uintptr_t>(push.row_shift * heads * head_dim * esz));
+  plan.lse = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(lse) -
+                                      static_cast<uintptr_t>(push.row_shift * 4));
+  plan.done_count = push.done_count;
+  plan.done_flag = push.done_flag;
+  plan.done_value = push.done_value;
   plan.tile_prefix[0] = 0;
   for (int i = 0; i < plan.nq; ++i)
     plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
-  if (sm100_supports(head_dim, heads, q, k, v, out) && plan.nkv > 0)
-    return launch_attn_sm100(q, k, v, tq_total, tk_total, head_dim, plan, s);
-  return launch_attn_simt(q, k, v, head_dim, plan, s);
+  if (sm100_supports(head_dim, heads, q, k, v, out) && plan.nkv > 0) {
+    // the kernel raises done_flag itself (last CTA); an empty grid does not run
+    if ((rc = launch_attn_sm100(q, k, v, tq_total, tk_total, head_dim, plan, s))) return rc;
+    return plan.tile_prefix[plan.nq] * heads == 0 ? flag_only() : TR_OK;
+  }
+  plan.done_flag = nullptr;          // the generic kernel signals with a trailing launch
+  if ((rc = launch_attn_simt(q, k, v, head_dim, plan, s))) return rc;
+  return flag_only();
 }
 
 }  // namespace tr
@@ -109,6 +136,29 @@ int tr_attention_segments(const void* q, const void* k, const void* v, void* out
                           int32_t n_kv, int32_t causal, int32_t out_dtype, void* stream) {
   return run_segments(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
                       n_kv, causal, out_dtype, static_cast<cudaStream_t>(stream));
+}
+
+int tr_attention_segments_push(const void* q, const void* k, const void* v, void* out, float* lse,
+                               int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
+                               const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
+                               int32_t n_kv, int32_t causal, int64_t row_shift, int64_t lse_stride,
+                               uint32_t* done_count, uint64_t* done_flag, uint64_t done_value,
+                               void* stream) {
+  if (!out || !lse) return fail(TR_ERR_INPUT, "null out/lse");
+  if (row_shift < 0 || lse_stride < 1) return fail(TR_ERR_DIMENSION, "row_shift >= 0, lse_stride >= 1 required");
+  if ((done_flag == nullptr) != (done_count == nullptr))
+    return fail(TR_ERR_INPUT, "done_flag and done_count go together");
+  for (int i = 0; i < n_q && i < TR_MAX_SEGMENTS; ++i)
+    if (q_segs[i].rows > 0 && (q_segs[i].row0 < row_shift || q_segs[i].row0 + q_segs[i].rows - row_shift > lse_stride))
+      return fail(TR_ERR_DIMENSION, "q segment rows fall outside the receive buffer");
+  PushOpts push;
+  push.row_shift = row_shift;
+  push.lse_stride = lse_stride;
+  push.done_count = done_count;
+  push.done_flag = reinterpret_cast<unsigned long long*>(done_flag);
+  push.done_value = done_value;
+  return run_segments(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
+                      n_kv, causal, TR_DTYPE_BF16, static_cast<cudaStream_t>(stream), push);
 }
 
 int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t blk_dtype,

@@ -26,12 +26,33 @@ struct AttnPlan {
   int32_t out_f32;   // out is float32 (an empty accumulator) instead of bf16
   void* out;
   float* lse;
+  // Fused OUT push (tr_attention_segments_push): out/lse may be a peer GPU's
+  // receive buffer (NVLink stores from the epilogue).  When done_flag is set,
+  // the last CTA to finish raises it to done_value (system-scope release)
+  // and resets done_count for the next launch on the stream.
+  unsigned int* done_count;
+  unsigned long long* done_flag;
+  unsigned long long done_value;
 };
+
+// last-CTA completion signal of a pushing launch (see AttnPlan::done_flag);
+// call from one thread per CTA after every thread of the CTA has executed
+// __threadfence_system() behind its out/lse stores and a __syncthreads().
+__device__ __forceinline__ void signal_done(const AttnPlan& p) {
+  const unsigned int prev = atomicAdd(p.done_count, 1u);
+  if (prev == gridDim.x - 1) {
+    *p.done_count = 0u;
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.done_flag), "l"(p.done_value)
+                 : "memory");
+  }
+}
 
 // tcgen05 kernel (D in {64,128}); returns TR_OK or an error status
 int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_total,
                       int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s);
 // generic CUDA-core kernel for any head_dim <= 256 (small shapes, odd dims)
+int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s);
 int launch_attn_simt(const void* q, const void* k, const void* v, int head_dim, AttnPlan& plan,
                      cudaStream_t s);
 bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const void* v,

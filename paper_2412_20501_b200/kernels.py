@@ -112,6 +112,41 @@ def attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse):
     return out, lse
 
 
+def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shift,
+                            done_count=None, done_flag=None, done_value=0):
+    """``attention_segments`` whose epilogue writes straight into a message
+    receive buffer -- typically the home rank's, mapped over CUDA IPC, so the
+    OUT_LSE message of the next step (ref engine.py:346-353) travels over
+    NVLink while the grid still computes.  ``out`` (n, H, D) bf16 and ``lse``
+    (H, n) float32 hold q rows [row_shift, row_shift + n).  With
+    ``done_flag`` (an int64 device tensor element, possibly a peer's) the
+    kernel's last CTA raises it to ``done_value``; ``done_count`` is a zeroed
+    int32 device counter owned by the caller's stream."""
+    _check_qkv(q, k, v)
+    _require_cuda("out", out, torch.bfloat16)
+    _require_cuda("lse", lse, torch.float32)
+    n = out.shape[0]
+    if out.dim() != 3 or out.shape[1:] != q.shape[1:] or lse.shape != (q.shape[1], n):
+        raise DimensionError("out/lse must be (n,H,D) / (H,n) with q's H and D")
+    for r0, rows, _ in q_segs:
+        if rows and (r0 < row_shift or r0 + rows - row_shift > n):
+            raise DimensionError(f"q rows [{r0}, {r0 + rows}) do not fit the receive buffer "
+                                 f"at shift {row_shift} (n={n})")
+    if (done_flag is None) != (done_count is None):
+        raise DimensionError("done_flag and done_count go together")
+    if done_flag is not None:
+        _require_cuda("done_flag", done_flag, torch.int64)
+        _require_cuda("done_count", done_count, torch.int32)
+    qs, ks = _segs(q_segs), _segs(kv_segs)
+    _lib.check(_lib.lib().tr_attention_segments_push(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
+        q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, row_shift, n,
+        None if done_count is None else _ptr(done_count),
+        None if done_flag is None else _ptr(done_flag), done_value, _stream(q.device)))
+    _count(1)
+    return out, lse
+
+
 def merge_state_(acc_out, acc_lse, blk_out, blk_lse, final_out=None):
     """In place: acc <- merge(acc, blk).  acc_out float32 (T,H,D); acc_lse /
     blk_lse may be column slices of wider (H, S) buffers (row stride S)."""

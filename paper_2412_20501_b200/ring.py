@@ -33,6 +33,13 @@ from .engine import MsgKind, build_token_ring, build_zigzag_token_ring, group_co
 from .errors import ConfigError, DimensionError, ScheduleError
 
 
+# nccl:  torch.distributed batch_isend_irecv on NCCL's streams
+# ipc:   copy engines into CUDA-IPC-mapped peer buffers + device sequence flags
+# fused: ipc for Q; the OUT_LSE messages are written by the attention kernel's
+#        epilogue straight into the home rank's receive slot (NVLink stores)
+TRANSPORTS = ("nccl", "ipc", "fused")
+
+
 class CudaOps:
     """Device ops of the product path (libtokenring.so)."""
 
@@ -122,6 +129,59 @@ def _rows(layout, ids, c):
     return idx[0] * c, (idx[0] + len(idx)) * c
 
 
+@dataclass
+class FusedPlan:
+    """Message bookkeeping of the ``fused`` transport for one rank.
+
+    push[s] = (msg, dst, row0, row1): computing step s writes its rows
+        [row0, row1) of the traveling-Q layout (all of them, in layout order)
+        straight into ``dst``'s receive slot msg % 2 -- the OUT_LSE message the
+        reference sends at step msg = s + 1 (engine.py:346-353).
+    recv[k] = (src, ids, slot): message k arrives in my slot k % 2; it is
+        merged at the start of step k + 1 (after the loop for the final phase),
+        as engine.py:187-200 wires the MergePlan.
+    grant_at_start: [(src, k)] -- the first message into each slot: its sender
+        may push as soon as the call starts.
+    grant_after[k] = (src, k2): after merging message k, slot k % 2 is free for
+        message k2 from src.
+    """
+    push: dict
+    recv: dict
+    grant_at_start: list
+    grant_after: dict
+
+
+def fused_plan(prog, c) -> FusedPlan:
+    """Derive the push/merge/grant program of one rank from its step program
+    (``compile_rank``); ScheduleError if a message is not a whole step's
+    rows (never the case for the reference's token-ring schedules)."""
+    push, recv = {}, {}
+    for k, st in enumerate(prog):
+        if st.send_out is not None:
+            dst, ids = st.send_out
+            prev = prog[k - 1]
+            if prev.accumulate or sorted(prev.q_ids) != sorted(ids):
+                raise ScheduleError(f"step {k}: OUT message {ids} is not step {k - 1}'s rows "
+                                    f"{prev.q_ids}; the fused transport cannot push it")
+            a, b = _rows(prev.q_layout, ids, c)
+            push[k - 1] = (k, dst, a, b)
+        if st.recv_out:
+            if len(st.recv_out) != 1:
+                raise ScheduleError(f"step {k}: more than one return per step")
+            src, ids = st.recv_out[0]
+            recv[k] = (src, tuple(ids), k % 2)
+    order = sorted(recv)
+    grant_at_start, grant_after, last_in_slot = [], {}, {}
+    for k in order:
+        src, _, slot = recv[k]
+        if slot in last_in_slot:
+            grant_after[last_in_slot[slot]] = (src, k)
+        else:
+            grant_at_start.append((src, k))
+        last_in_slot[slot] = k
+    return FusedPlan(push, recv, grant_at_start, grant_after)
+
+
 class TokenRingAttention:
     """TokenRing forward on this process's rank of ``group``.
 
@@ -160,11 +220,12 @@ class TokenRingAttention:
         self.device = self.ops.device
         self.record_timeline = record_timeline
         self.timeline = []
-        if transport not in ("nccl", "ipc"):
-            raise ConfigError(f"transport must be 'nccl' or 'ipc', got {transport!r}")
+        if transport not in TRANSPORTS:
+            raise ConfigError(f"transport must be one of {TRANSPORTS}, got {transport!r}")
         self.transport = transport if self.P > 1 else "nccl"
+        self.fplan = fused_plan(self.prog, self.c) if self.transport == "fused" else None
         self._alloc()
-        if self.transport == "ipc":
+        if self.transport in ("ipc", "fused"):
             self._ipc_setup()
 
     def _alloc(self):
@@ -178,6 +239,12 @@ class TokenRingAttention:
         self.lse_recv = torch.empty((H, rows), dtype=torch.float32, device=dev)
         self.acc_out = torch.empty((rows, H, D), dtype=torch.float32, device=dev)
         self.acc_lse = torch.empty((H, rows), dtype=torch.float32, device=dev)
+        if self.transport == "fused":
+            # second receive slot (messages alternate slots by step parity) and
+            # the launch counter the pushing kernels use for their done flag
+            self.out_recv2 = torch.empty((rows, H, D), dtype=bf, device=dev)
+            self.lse_recv2 = torch.empty((H, rows), dtype=torch.float32, device=dev)
+            self.done_count = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # -- transport -----------------------------------------------------------
     def _comm(self, sends, recvs):
@@ -208,11 +275,18 @@ class TokenRingAttention:
     #   flags[3] o_free  : highest step whose returned OUT I have merged
     #   flags[4+s] q_ready from s: highest step whose Q from rank s has landed
     #              (one per source: the direct route has two Q senders per step)
+    # fused transport (OUT pushed by the attention epilogue) adds
+    #   flags[4+P+s]   o_ready of receive slot s (raised by the pushing kernel)
+    #   flags[6+P+k]   push grant for message k (raised by its home, once the
+    #                  slot the message lands in has been merged)
     def _ipc_setup(self):
         from torch.multiprocessing.reductions import reduce_tensor
-        self.flags = torch.zeros(4 + self.P, dtype=torch.int64, device=self.device)
-        mine = [reduce_tensor(t) for t in (self.qbuf[0], self.qbuf[1], self.out_recv,
-                                           self.lse_recv, self.flags)]
+        self.flags = torch.zeros(4 + self.P + 2 + len(self.prog) + 1, dtype=torch.int64,
+                                 device=self.device)
+        shared = [self.qbuf[0], self.qbuf[1], self.out_recv, self.lse_recv, self.flags]
+        if self.transport == "fused":
+            shared += [self.out_recv2, self.lse_recv2]
+        mine = [reduce_tensor(t) for t in shared]
         everyone = [None] * self.P
         dist.all_gather_object(everyone, mine, group=self.group)
         self.peer = {}
@@ -224,8 +298,20 @@ class TokenRingAttention:
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.calls = 0
 
+    def _flags_of(self, r):
+        return self.flags if r == self.rank else self.peer[r][4]
+
+    def _recv_slot(self, slot, r=None):
+        """(out, lse) receive buffers of slot 0/1 -- mine, or peer r's."""
+        if r is None or r == self.rank:
+            return (self.out_recv, self.lse_recv) if slot == 0 else (self.out_recv2, self.lse_recv2)
+        p = self.peer[r]
+        return (p[2], p[3]) if slot == 0 else (p[5], p[6])
+
     def _forward_ipc(self, q_loc, k_loc, v_loc) -> Partial:
-        c, rank, P = self.c, self.rank, self.P
+        c, rank, P, H = self.c, self.rank, self.P, self.H
+        fused, fp = self.transport == "fused", self.fplan
+        O0, G0 = 4 + P, 6 + P          # fused: o_ready slots, push grants
         base = self.calls * (P + 4) + 8
         self.calls += 1
         cur = torch.cuda.current_stream(self.device)
@@ -235,6 +321,9 @@ class TokenRingAttention:
         self.flags[4:] = base - 1
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
+        if fused:
+            for src, k in fp.grant_at_start:      # my empty slots: their first messages may go
+                kernels.flag_set_(self._flags_of(src)[G0 + k:G0 + k + 1], base + k, cur)
         if not self.direct_first:
             self.ops.init_(self.acc_out, self.acc_lse)
         local_layout = self.prog[0].q_layout
@@ -250,7 +339,8 @@ class TokenRingAttention:
                 for src, _ in self.prog[i - 1].recv_q:                  # Q_i has landed
                     kernels.flag_wait_(self.flags[4 + src:5 + src], base + i, cur)
             if i >= 1 and self.prog[i - 1].recv_out:
-                kernels.flag_wait_(self.flags[2:3], base + i - 1, cur)
+                o = O0 + (i - 1) % 2 if fused else 2
+                kernels.flag_wait_(self.flags[o:o + 1], base + i - 1, cur)
             if self.record_timeline:
                 ev["comm_ready"] = self.ops.event()
                 self.ops.record(ev["comm_ready"])
@@ -258,10 +348,14 @@ class TokenRingAttention:
                 # OUT sent to me at step i-1 has landed: merge it, free the buffer
                 src, ids = self.prog[i - 1].recv_out[0]
                 n = len(ids) * c
-                self._merge_returned((ids, self.out_recv[:n],
-                                      self.lse_recv.view(-1)[: self.H * n].view(self.H, n)),
+                ob, lb = self._recv_slot((i - 1) % 2 if fused else 0)
+                self._merge_returned((ids, ob[:n], lb.view(-1)[: H * n].view(H, n)),
                                      local_layout)
-                kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
+                if not fused:
+                    kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
+                elif (i - 1) in fp.grant_after:   # slot free: grant the next message into it
+                    s2, k2 = fp.grant_after[i - 1]
+                    kernels.flag_set_(self._flags_of(s2)[G0 + k2:G0 + k2 + 1], base + k2, cur)
             cur_q = self.qbuf[i % 2] if i > 0 else q_loc
             ev_q = torch.cuda.Event()
             ev_q.record(cur)
@@ -274,7 +368,7 @@ class TokenRingAttention:
                 kernels.flag_wait_(self.peer[dst][4][1:2], base + i - 1, cs)   # peer slot free
                 kernels.copy_(self.peer[dst][(i + 1) % 2][d0:d1], src_buf[a:b], cs)
                 kernels.flag_set_(self.peer[dst][4][4 + rank:5 + rank], base + i + 1, cs)
-            if st.send_out is not None:
+            if st.send_out is not None and not fused:   # fused: pushed by step i-1's kernel
                 dst, ids = st.send_out
                 a, b = _rows(self.prog[i - 1].q_layout, ids, c)
                 cs.wait_event(ev_comp[i - 1])
@@ -296,12 +390,36 @@ class TokenRingAttention:
                 kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
                             self.sched.chunks[b].start) for b in st.kv_ids]
                 buf = i % 2
+                if fused and i in fp.push:
+                    # the home's grant for my push (it has merged the previous
+                    # message in that slot) -- after my own merge above, so the
+                    # ranks never wait on each other in a cycle
+                    k = fp.push[i][0]
+                    if self.record_timeline:
+                        ev["grant_wait"] = self.ops.event()
+                        self.ops.record(ev["grant_wait"])
+                    kernels.flag_wait_(self.flags[G0 + k:G0 + k + 1], base + k, cur)
+                    if self.record_timeline:
+                        ev["granted"] = self.ops.event()
+                        self.ops.record(ev["granted"])
                 if self.record_timeline:
                     ev["attn_start"] = self.ops.event()
                     self.ops.record(ev["attn_start"])
                 if i == 0 and self.direct_first:
                     self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
                                        self.acc_out, self.acc_lse)
+                elif fused and i in fp.push:
+                    # compute + send in one kernel: rows go straight into the
+                    # home's receive slot over NVLink; its last CTA raises the
+                    # home's o_ready flag
+                    k, dst, a, b = fp.push[i]
+                    ob, lb = self._recv_slot(k % 2, dst)
+                    n = b - a
+                    o = O0 + k % 2
+                    kernels.attention_segments_push(
+                        cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal, ob[:n],
+                        lb.view(-1)[: H * n].view(H, n), a, self.done_count,
+                        self._flags_of(dst)[o:o + 1], base + k)
                 else:
                     self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
                                        self.obuf[buf], self.lbuf[buf])
@@ -328,17 +446,17 @@ class TokenRingAttention:
                 kernels.flag_set_(self.flags[1:2], base + i, cs)
         last = self.prog[-1]
         if last.recv_out:
-            kernels.flag_wait_(self.flags[2:3], base + last.step, cur)
+            o = O0 + last.step % 2 if fused else 2
+            kernels.flag_wait_(self.flags[o:o + 1], base + last.step, cur)
             src, ids = last.recv_out[0]
             n = len(ids) * c
-            self._merge_returned((ids, self.out_recv[:n],
-                                  self.lse_recv.view(-1)[: self.H * n].view(self.H, n)),
-                                 local_layout)
+            ob, lb = self._recv_slot(last.step % 2 if fused else 0)
+            self._merge_returned((ids, ob[:n], lb.view(-1)[: H * n].view(H, n)), local_layout)
         cur.wait_stream(cs)
         return Partial(self.acc_out, self.acc_lse)
 
     def __call__(self, q_loc, k_loc, v_loc) -> Partial:
-        if self.transport == "ipc":
+        if self.transport in ("ipc", "fused"):
             shape = (self.local_rows, self.H, self.D)
             for n, t in (("q", q_loc), ("k", k_loc), ("v", v_loc)):
                 if tuple(t.shape) != shape:

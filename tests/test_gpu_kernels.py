@@ -9,6 +9,7 @@ import torch
 
 from oracle import kernels as ok
 from oracle import splitmix
+from paper_2412_20501_b200.errors import DimensionError
 
 pytestmark = pytest.mark.gpu
 
@@ -155,6 +156,40 @@ def test_segments_float32_out(K, d):
     err32 = np.abs(o32[c:].double().cpu().numpy() - ref_o).max()
     err16 = np.abs(o16[c:].double().cpu().numpy() - ref_o).max()
     assert err32 <= err16 + 1e-6 and err32 <= 5e-3, (err32, err16)
+
+
+@pytest.mark.parametrize("d", [128, 64, 32])
+def test_segments_push_into_message_buffer(K, d):
+    """tr_attention_segments_push: the rows of q segment(s) [c, 3c) land at
+    rows [0, 2c) of a message-sized buffer (row shift c, lse stride 2c),
+    bit-identical to the local launch; the done flag is raised to the given
+    value by the kernel (simt path for d=32: by the trailing flag launch),
+    the counter is left at zero, and repeated launches reuse it."""
+    c, h = 256, 2
+    S = 4 * c
+    q, k, v = (dev(x) for x in splitmix.attention_inputs(30 + d, S, h, d))
+    qs = [(c, c, c), (2 * c, c, 2 * c)]
+    ks = [(0, S, 0)]
+    ref_o = torch.zeros((S, h, d), dtype=torch.bfloat16, device="cuda")
+    ref_l = torch.zeros((h, S), dtype=torch.float32, device="cuda")
+    K.attention_segments(q, k, v, qs, ks, True, ref_o, ref_l)
+    flag = torch.zeros(3, dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for it in range(3):
+        out = torch.full((2 * c, h, d), 5.0, dtype=torch.bfloat16, device="cuda")
+        lse = torch.full((h, 2 * c), 5.0, dtype=torch.float32, device="cuda")
+        K.attention_segments_push(q, k, v, qs, ks, True, out, lse, c, cnt, flag[1:2], 40 + it)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_o[c:3 * c]) and torch.equal(lse, ref_l[:, c:3 * c])
+        assert flag.tolist() == [0, 40 + it, 0] and cnt.item() == 0
+    # no flag: plain shifted write
+    out = torch.zeros((2 * c, h, d), dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros((h, 2 * c), dtype=torch.float32, device="cuda")
+    K.attention_segments_push(q, k, v, qs, ks, True, out, lse, c)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref_o[c:3 * c])
+    with pytest.raises(DimensionError):          # rows below the shift cannot be written
+        K.attention_segments_push(q, k, v, [(0, c, 0)], ks, True, out, lse, c)
 
 
 def test_merge_golden(K, golden_merge):

@@ -1,6 +1,8 @@
 """Multi-process TokenRing on the GPU with the copy-engine (CUDA IPC)
-transport: 2 and 4 ranks as separate processes sharing cuda:0 (gloo only for
-the one-time handle exchange and barriers), checked against the oracle's
+transport and the fused transport (OUT rows pushed by the attention kernel's
+epilogue into the home rank's IPC-mapped receive slot): 2, 3 and 4 ranks as
+separate processes sharing cuda:0 (gloo only for the one-time handle
+exchange and barriers), checked against the oracle's
 execute of the same schedule.  Exercises real cross-process device memory
 writes, sequence flags and stream ordering -- the same code path as one rank
 per GPU over NVLink, minus the link."""
@@ -29,7 +31,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, S, H, D, causal, calls, q_out, route):
+def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -38,7 +40,7 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route):
         from paper_2412_20501_b200 import rng
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
-                                    transport="ipc", route=route)
+                                    transport=transport, route=route)
         q, k, v = rng.local_inputs(21, runner.part, rank, H, D)
         for _ in range(calls):            # repeated calls exercise the flag bases
             res = runner(q, k, v)
@@ -49,14 +51,18 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,S,H,D,causal,route", [
-    (2, 2048, 2, 128, True, "ring"), (4, 4096, 2, 128, True, "ring"), (2, 1024, 2, 64, False, "ring"),
-    (4, 4096, 2, 128, True, "direct")])
-def test_token_ring_ipc(world, S, H, D, causal, route):
+@pytest.mark.parametrize("world,S,H,D,causal,route,transport", [
+    (2, 2048, 2, 128, True, "ring", "ipc"), (4, 4096, 2, 128, True, "ring", "ipc"),
+    (2, 1024, 2, 64, False, "ring", "ipc"), (4, 4096, 2, 128, True, "direct", "ipc"),
+    (2, 2048, 2, 128, True, "ring", "fused"), (4, 4096, 2, 128, True, "ring", "fused"),
+    (3, 3072, 2, 64, False, "ring", "fused"), (4, 4096, 2, 128, True, "direct", "fused"),
+    (3, 1536, 2, 96, True, "ring", "fused")])
+def test_token_ring_ipc(world, S, H, D, causal, route, transport):
     ctx = mp.get_context("spawn")
     q_out = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, S, H, D, causal, 3, q_out, route))
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, S, H, D, causal, 3, q_out, route, transport))
              for r in range(world)]
     for p in procs:
         p.start()
