@@ -49,10 +49,11 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc", "fused"],
-                    help="N>1 exchange: NCCL P2P (default), copy-engine CUDA IPC, or fused "
-                         "(IPC for Q, OUT rows stored by the attention epilogue into the "
-                         "home rank's buffer)")
+    ap.add_argument("--transport", default="fused", choices=["nccl", "ipc", "fused"],
+                    help="N>1 exchange: fused (default: Q by copy engines into the peer's "
+                         "IPC-mapped buffer, OUT rows stored by the attention epilogue straight "
+                         "into the home rank's receive slot), ipc (copy engines both ways) or "
+                         "nccl (torch.distributed P2P, the baseline)")
     return ap.parse_args()
 
 
@@ -409,7 +410,8 @@ def run_ours(a):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (SplitMix64 uniform[-1,1) -> bf16, seed {a.seed}, generated on "
                     "device per rank shard)",
-            "config": dict(workload_config(a, world), transport=a.transport,
+            "config": dict(workload_config(a, world),
+                           transport=runner.transport if world > 1 else "none (1 rank)",
                            **({"test_mode": "all ranks share cuda:0 (TR_BENCH_SHARED_DEVICE)"}
                               if shared else {})),
             "tokens_per_s": S / (ms * 1e-3),

@@ -127,6 +127,11 @@ int tr_splitmix_bf16(uint64_t seed, int64_t first, int64_t count, double low, do
 int tr_flag_set(uint64_t* flag, uint64_t value, void* stream);
 int tr_flag_wait(const uint64_t* flag, uint64_t value, void* stream);
 int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
+/* Let kernels of the calling thread's current device load/store memory of
+ * peer_device (flags, receive slots mapped over CUDA IPC): wraps
+ * cudaDeviceEnablePeerAccess; TR_OK if already enabled or the same device,
+ * TR_ERR_UNSUPPORTED if the two devices have no P2P path. */
+int tr_enable_peer_access(int32_t peer_device);
 
 /* Version / capability probes (no GPU work). */
 const char* tr_version(void);

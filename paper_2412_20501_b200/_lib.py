@@ -28,7 +28,8 @@ TR_DTYPE_BF16 = 1
 # every symbol include/tokenring.h declares
 EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
            "tr_merge_state", "tr_partial_init",
-           "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_copy_async", "tr_version",
+           "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_copy_async",
+           "tr_enable_peer_access", "tr_version",
            "tr_kernel_count", "tr_last_error")
 
 
@@ -66,10 +67,11 @@ def _declare(lib):
     lib.tr_flag_set.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tr_flag_wait.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tr_copy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
+    lib.tr_enable_peer_access.argtypes = [i32]
     for name in ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
                  "tr_merge_state",
                  "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
-                 "tr_copy_async"):
+                 "tr_copy_async", "tr_enable_peer_access"):
         getattr(lib, name).restype = ctypes.c_int
     lib.tr_version.restype = ctypes.c_char_p
     lib.tr_version.argtypes = []

@@ -206,6 +206,25 @@ int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
                      "tr_copy_async");
 }
 
+int tr_enable_peer_access(int32_t peer_device) {
+  int cur = 0;
+  int rc = cuda_status(cudaGetDevice(&cur), "cudaGetDevice");
+  if (rc) return rc;
+  if (peer_device == cur) return TR_OK;
+  int can = 0;
+  if ((rc = cuda_status(cudaDeviceCanAccessPeer(&can, cur, peer_device), "cudaDeviceCanAccessPeer")))
+    return rc;
+  if (!can)
+    return fail(TR_ERR_UNSUPPORTED, "device " + std::to_string(cur) + " cannot access device " +
+                                        std::to_string(peer_device) + " (no P2P path)");
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();   // clear the sticky-free status
+    return TR_OK;
+  }
+  return cuda_status(e, "cudaDeviceEnablePeerAccess");
+}
+
 const char* tr_version(void) { return "tokenring-b200 0.1 (sm_100a)"; }
 int32_t tr_kernel_count(void) { return 9; }
 const char* tr_last_error(void) { return g_last_error.c_str(); }

@@ -225,3 +225,9 @@ def copy_(dst, src, stream=None):
     s = stream or torch.cuda.current_stream(src.device)
     _lib.check(_lib.lib().tr_copy_async(_ptr(dst), _ptr(src), dst.numel() * dst.element_size(),
                                         ctypes.c_void_p(s.cuda_stream)))
+
+
+def enable_peer_access(peer_device):
+    """Let kernels on the current device dereference ``peer_device`` memory
+    (IPC-mapped flags / receive slots of the ipc and fused transports)."""
+    _lib.check(_lib.lib().tr_enable_peer_access(int(peer_device)))

@@ -295,6 +295,12 @@ class TokenRingAttention:
                 continue
             fn_args = everyone[r]
             self.peer[r] = [fn(*args) for fn, args in fn_args]
+            # torch maps a peer's handles in the PEER device's context; our flag
+            # and push kernels run on this device and dereference them directly
+            peer_dev = self.peer[r][0].device.index
+            if peer_dev != self.device.index:
+                with torch.cuda.device(self.device):
+                    kernels.enable_peer_access(peer_dev)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.calls = 0
 

@@ -33,7 +33,8 @@ def test_header_declares_expected_api():
     assert fns == sorted(["tr_attention_block", "tr_attention_segments",
                           "tr_attention_segments_push", "tr_merge_state",
                           "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
-                          "tr_copy_async", "tr_version", "tr_kernel_count", "tr_last_error"])
+                          "tr_copy_async", "tr_enable_peer_access", "tr_version",
+                          "tr_kernel_count", "tr_last_error"])
 
 
 def test_library_exports_every_declared_symbol(lib):
