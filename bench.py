@@ -298,6 +298,30 @@ def e2e_pipelined(runner, q, k, v, steps, barrier, allmax):
     return allmax([s.elapsed_time(e) / steps])[0]
 
 
+def exchange_report(world, runner, xsum, n_fwd, shared):
+    """Per-direction exchange of the TokenRing schedule (Q
+    forward, OUT_LSE reverse) in GB/s against NVLink 5's 900 GB/s per
+    direction.  Bytes are algorithmic (Q: rows*H*D*2, OUT: rows*H*(2D+4)),
+    summed over all ranks; time is the device time of the transfers."""
+    if world == 1:
+        return None
+    q_b, q_ms, o_b, o_ms = xsum
+    fwd = max(1, n_fwd)
+    rep = {"peak_gbs_per_direction": 900.0,
+           "q_bytes_per_forward": q_b / fwd, "out_bytes_per_forward": o_b / fwd,
+           "q_gbs": q_b / (q_ms * 1e-3) / 1e9 if q_ms > 0 else None,
+           "out_gbs": o_b / (o_ms * 1e-3) / 1e9 if o_ms > 0 else None,
+           "transport": runner.transport}
+    if runner.transport == "fused":
+        rep["out_path"] = ("epilogue stores into the home's slot; out_gbs = bytes over the "
+                           "launch that computes them (link load, not link peak)")
+    if runner.transport == "nccl":
+        rep["note"] = "NCCL P2P runs on NCCL's streams; only exposed comm is timed"
+    if shared:
+        rep["note"] = "all ranks share one GPU: copies are device-local, not NVLink"
+    return rep
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -320,6 +344,13 @@ def run_ours(a):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def allsum(vals):
+        if world == 1:
+            return list(vals)
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return [float(x) for x in t.tolist()]
 
     def allmax(vals):
         if world == 1:
@@ -380,6 +411,22 @@ def run_ours(a):
                 kern_ms += ev["attn_start"].elapsed_time(ev["attn_end"])
                 kern_flops += ev["attn_flops"]
                 nlaunch += 1
+    # exchange: copy-engine transfers timed on the copy stream (ipc: Q and
+    # OUT; fused: Q, while OUT rides inside the attention launch that
+    # computes it, so its rate is the bytes over that launch's time)
+    xq_b = xq_ms = xo_b = xo_ms = 0.0
+    for tl in timelines:
+        for ev in tl:
+            for e0, e1, nb in ev.get("q_copies", ()):
+                xq_b += nb
+                xq_ms += e0.elapsed_time(e1)
+            for e0, e1, nb in ev.get("o_copies", ()):
+                xo_b += nb
+                xo_ms += e0.elapsed_time(e1)
+            if "o_push_bytes" in ev:
+                xo_b += ev["o_push_bytes"]
+                xo_ms += ev["attn_start"].elapsed_time(ev["attn_end"])
+    xsum = allsum([xq_b, xq_ms, xo_b, xo_ms])
     exposed = stall / max(1, len(timelines))
     attn_avg_ms = kern_ms / max(1, nlaunch)
     attn_flops_per_launch = kern_flops / max(1, nlaunch)
@@ -416,6 +463,7 @@ def run_ours(a):
                               if shared else {})),
             "tokens_per_s": S / (ms * 1e-3),
             "exposed_comm_ms_per_step": exposed,
+            "exchange": exchange_report(world, runner, xsum, len(timelines), shared),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(),

@@ -22,6 +22,7 @@ what ref ``engine.execute`` returns per rank, so ``global_reorder`` works.
 
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass
 
 import torch
@@ -314,6 +315,18 @@ class TokenRingAttention:
         p = self.peer[r]
         return (p[2], p[3]) if slot == 0 else (p[5], p[6])
 
+    @contextlib.contextmanager
+    def _timed_copy(self, ev, key, stream, nbytes):
+        """Timeline events around a copy-engine transfer on ``stream``."""
+        if not self.record_timeline:
+            yield
+            return
+        e0, e1 = self.ops.event(), self.ops.event()
+        e0.record(stream)
+        yield
+        e1.record(stream)
+        ev.setdefault(key, []).append((e0, e1, nbytes))
+
     def _forward_ipc(self, q_loc, k_loc, v_loc) -> Partial:
         c, rank, P, H = self.c, self.rank, self.P, self.H
         fused, fp = self.transport == "fused", self.fplan
@@ -372,7 +385,8 @@ class TokenRingAttention:
                 a, b = _rows(src_layout, ids, c)
                 d0, d1 = _rows(self._next_layout(dst, i), ids, c)
                 kernels.flag_wait_(self.peer[dst][4][1:2], base + i - 1, cs)   # peer slot free
-                kernels.copy_(self.peer[dst][(i + 1) % 2][d0:d1], src_buf[a:b], cs)
+                with self._timed_copy(ev, "q_copies", cs, (b - a) * H * self.D * 2):
+                    kernels.copy_(self.peer[dst][(i + 1) % 2][d0:d1], src_buf[a:b], cs)
                 kernels.flag_set_(self.peer[dst][4][4 + rank:5 + rank], base + i + 1, cs)
             if st.send_out is not None and not fused:   # fused: pushed by step i-1's kernel
                 dst, ids = st.send_out
@@ -383,8 +397,9 @@ class TokenRingAttention:
                 ls = self.lse_send.view(-1)[: self.H * (b - a)].view(self.H, b - a)
                 with torch.cuda.stream(cs):
                     ls.copy_(lb[:, a:b])
-                kernels.copy_(self.peer[dst][2][: b - a], ob[a:b], cs)
-                kernels.copy_(self.peer[dst][3].view(-1)[: self.H * (b - a)], ls, cs)
+                with self._timed_copy(ev, "o_copies", cs, (b - a) * H * (2 * self.D + 4)):
+                    kernels.copy_(self.peer[dst][2][: b - a], ob[a:b], cs)
+                    kernels.copy_(self.peer[dst][3].view(-1)[: self.H * (b - a)], ls, cs)
                 kernels.flag_set_(self.peer[dst][4][2:3], base + i, cs)
                 ev_out_sent[i] = torch.cuda.Event()
                 ev_out_sent[i].record(cs)
@@ -421,6 +436,7 @@ class TokenRingAttention:
                     k, dst, a, b = fp.push[i]
                     ob, lb = self._recv_slot(k % 2, dst)
                     n = b - a
+                    ev["o_push_bytes"] = n * H * (2 * self.D + 4)   # carried by this launch
                     o = O0 + k % 2
                     kernels.attention_segments_push(
                         cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal, ob[:n],
