@@ -363,8 +363,20 @@ def run_ours(a):
     from paper_2412_20501_b200.ring import TokenRingAttention
 
     S, H, D = a.seq, a.heads, a.head_dim
+    transport = a.transport
+    if world > 1 and not shared and transport in ("ipc", "fused"):
+        # peer-memory transports need a P2P path between every pair of GPUs;
+        # decide collectively so every rank runs the same transport
+        n = torch.cuda.device_count()
+        ok = all(torch.cuda.can_device_access_peer(dev_index, d) for d in range(n) if d != dev_index)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if flag.item() == 0:
+            print(f"bench: no P2P path between all GPUs; transport {transport} -> nccl",
+                  file=sys.stderr)
+            transport = "nccl"
     runner = TokenRingAttention(S, H, D, causal=True, record_timeline=True,
-                                transport=a.transport)
+                                transport=transport)
     q, k, v = rng.local_inputs(a.seed, runner.part, rank, H, D)
     total_flops = causal_flops(S, H, D)
 

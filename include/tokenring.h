@@ -108,6 +108,19 @@ int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t 
                    int64_t acc_lse_stride, int64_t blk_lse_stride, void* final_out,
                    void* stream);
 
+/* N-way form of tr_merge_state: acc <- merge(acc, blk_0, ..., blk_{n-1}) in one
+ * pass (every MergePlan a chunk receives over the schedule, engine.py:187-200
+ * and 620-628, folded at once -- the merge is associative and commutative).
+ * blk_out[i] points at `tokens` rows (T, H, D) of dtype blk_dtype;
+ * blk_lse[i] at an (H, .) float32 array with row stride blk_lse_stride[i].
+ * The pointer arrays are host memory; n_blk <= TR_MERGE_MAX.  If final_out !=
+ * NULL the merged output is also written there as bf16. */
+#define TR_MERGE_MAX 16
+int tr_merge_n(float* acc_out, float* acc_lse, int64_t acc_lse_stride, const void* const* blk_out,
+               int32_t blk_dtype, const float* const* blk_lse, const int64_t* blk_lse_stride,
+               int32_t n_blk, int64_t tokens, int32_t heads, int32_t head_dim, void* final_out,
+               void* stream);
+
 /* Identity accumulator (Partial.empty, ref core.py:75-78): out = 0, lse = -inf. */
 int tr_partial_init(float* acc_out, float* acc_lse, int64_t tokens, int32_t heads,
                     int32_t head_dim, void* stream);

@@ -24,10 +24,11 @@ TR_ERR_UNSUPPORTED = -5
 
 TR_DTYPE_F32 = 0
 TR_DTYPE_BF16 = 1
+TR_MERGE_MAX = 16
 
 # every symbol include/tokenring.h declares
 EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
-           "tr_merge_state", "tr_partial_init",
+           "tr_merge_state", "tr_merge_n", "tr_partial_init",
            "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_copy_async",
            "tr_enable_peer_access", "tr_version",
            "tr_kernel_count", "tr_last_error")
@@ -61,6 +62,8 @@ def _declare(lib):
                                                ctypes.POINTER(Segment), i32, i32, i64, i64,
                                                vp, vp, ctypes.c_uint64, vp]
     lib.tr_merge_state.argtypes = [vp, vp, vp, i32, vp, i64, i32, i32, i64, i64, vp, vp]
+    lib.tr_merge_n.argtypes = [vp, vp, i64, ctypes.POINTER(vp), i32, ctypes.POINTER(vp),
+                               ctypes.POINTER(i64), i32, i64, i32, i32, vp, vp]
     lib.tr_partial_init.argtypes = [vp, vp, i64, i32, i32, vp]
     lib.tr_splitmix_bf16.argtypes = [ctypes.c_uint64, i64, i64, ctypes.c_double,
                                      ctypes.c_double, vp, vp]
@@ -69,7 +72,7 @@ def _declare(lib):
     lib.tr_copy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
     lib.tr_enable_peer_access.argtypes = [i32]
     for name in ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
-                 "tr_merge_state",
+                 "tr_merge_state", "tr_merge_n",
                  "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
                  "tr_copy_async", "tr_enable_peer_access"):
         getattr(lib, name).restype = ctypes.c_int

@@ -25,6 +25,9 @@ int cuda_status(cudaError_t e, const char* what) {
 int launch_merge(float* acc_out, float* acc_lse, const void* blk_out, int blk_dtype,
                  const float* blk_lse, int64_t T, int H, int D, int64_t als, int64_t bls,
                  void* fin, cudaStream_t s);
+int launch_merge_n(float* acc_out, float* acc_lse, int64_t als, const void* const* blk,
+                   int blk_dtype, const float* const* blk_lse, const int64_t* bls, int n,
+                   int64_t T, int H, int D, void* fin, cudaStream_t s);
 int launch_partial_init(float* acc_out, float* acc_lse, int64_t T, int H, int D, cudaStream_t s);
 int launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 int launch_splitmix(uint64_t seed, int64_t first, int64_t count, double low, double high,
@@ -170,6 +173,20 @@ int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t 
     return fail(TR_ERR_DIMENSION, "lse row stride smaller than the token count");
   return launch_merge(acc_out, acc_lse, blk_out, blk_dtype, blk_lse, tokens, heads, head_dim,
                       acc_lse_stride, blk_lse_stride, final_out, static_cast<cudaStream_t>(stream));
+}
+
+int tr_merge_n(float* acc_out, float* acc_lse, int64_t acc_lse_stride, const void* const* blk_out,
+               int32_t blk_dtype, const float* const* blk_lse, const int64_t* blk_lse_stride,
+               int32_t n_blk, int64_t tokens, int32_t heads, int32_t head_dim, void* final_out,
+               void* stream) {
+  if (tokens < 0 || heads < 1 || head_dim < 1)
+    return fail(TR_ERR_DIMENSION, "tokens >= 0, heads >= 1, head_dim >= 1 required");
+  if (acc_lse_stride < tokens) return fail(TR_ERR_DIMENSION, "lse row stride smaller than the token count");
+  if (n_blk > 0 && (!blk_out || !blk_lse || !blk_lse_stride))
+    return fail(TR_ERR_INPUT, "null block arrays");
+  return launch_merge_n(acc_out, acc_lse, acc_lse_stride, blk_out, blk_dtype, blk_lse,
+                        blk_lse_stride, n_blk, tokens, heads, head_dim, final_out,
+                        static_cast<cudaStream_t>(stream));
 }
 
 int tr_partial_init(float* acc_out, float* acc_lse, int64_t tokens, int32_t heads,

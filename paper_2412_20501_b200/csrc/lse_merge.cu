@@ -140,6 +140,176 @@ __global__ void merge_scalar_lse_kernel(float* acc_lse, const float* blk_lse, in
   acc_lse[h * acc_ls + t] = fmaxf(a, b) + log1pf(e);
 }
 
+// ---------------------------------------------------------------- N-way merge
+// acc <- merge(acc, blk_0, ..., blk_{n-1}) in one pass: the reference folds
+// returned partials one MergePlan at a time (engine.py:187-200, 620-628);
+// the merge is associative and commutative (ref tests/test_core.py:151-173),
+// so all of a row's partials are combined with one set of weights:
+//   m = max(a, b_i),  w = exp(a - m), w_i = exp(b_i - m),  L = w + sum w_i
+//   out = (w acc + sum w_i blk_i) / L,   lse = m + log L
+// (-inf partials get weight 0; a row with every lse -inf stays 0 / -inf).
+// HBM traffic per value: 4 (acc read) + n * sizeof(blk) + 4 (acc write),
+// against n * (4 + sizeof(blk) + 4) for n pairwise merges.
+struct MergeN {
+  const void* blk[TR_MERGE_MAX];
+  const float* lse[TR_MERGE_MAX];
+  int64_t ls[TR_MERGE_MAX];
+  int n;
+};
+
+template <typename BT>
+__global__ void __launch_bounds__(256) merge_n_vec8_kernel(float* __restrict__ acc_out,
+                                                           const float* __restrict__ acc_lse,
+                                                           const __grid_constant__ MergeN m,
+                                                           int64_t T, int H, int D, int64_t acc_ls,
+                                                           __nv_bfloat16* __restrict__ final_out) {
+  const int per_row = D / 8;
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gid / per_row;  // head-major row index
+  if (row >= T * H) return;
+  const int part = static_cast<int>(gid % per_row);
+  const int h = static_cast<int>(row / T);
+  const int64_t t = row % T;
+  const float a = acc_lse[h * acc_ls + t];
+  float mx = a;
+  float b[TR_MERGE_MAX];
+#pragma unroll
+  for (int i = 0; i < TR_MERGE_MAX; ++i) {
+    b[i] = i < m.n ? __ldg(m.lse[i] + h * m.ls[i] + t) : -INFINITY;
+    mx = fmaxf(mx, b[i]);
+  }
+  const int64_t off = (t * H + h) * D + part * 8;
+  float* ap = acc_out + off;
+  if (mx == -INFINITY) {          // nothing anywhere: the identity stays
+    if (final_out) *reinterpret_cast<uint4*>(final_out + off) = make_uint4(0u, 0u, 0u, 0u);
+    return;
+  }
+  float o[8];
+  const float w0 = (a == -INFINITY) ? 0.f : __expf(a - mx);
+  float L = w0;
+  if (w0 != 0.f) {
+    const float4 x0 = *reinterpret_cast<const float4*>(ap);
+    const float4 x1 = *(reinterpret_cast<const float4*>(ap) + 1);
+    o[0] = w0 * x0.x; o[1] = w0 * x0.y; o[2] = w0 * x0.z; o[3] = w0 * x0.w;
+    o[4] = w0 * x1.x; o[5] = w0 * x1.y; o[6] = w0 * x1.z; o[7] = w0 * x1.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < TR_MERGE_MAX; ++i) {
+    if (i >= m.n) break;
+    if (b[i] == -INFINITY) continue;
+    const float w = __expf(b[i] - mx);
+    L += w;
+    float x[8];
+    Vec8<BT>::load(static_cast<const BT*>(m.blk[i]) + off, x);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = fmaf(w, x[k], o[k]);
+  }
+  const float inv = 1.f / L;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o[k] *= inv;
+  reinterpret_cast<float4*>(ap)[0] = make_float4(o[0], o[1], o[2], o[3]);
+  reinterpret_cast<float4*>(ap)[1] = make_float4(o[4], o[5], o[6], o[7]);
+  if (final_out)
+    *reinterpret_cast<uint4*>(final_out + off) =
+        make_uint4(bf16x2(o[0], o[1]), bf16x2(o[2], o[3]), bf16x2(o[4], o[5]), bf16x2(o[6], o[7]));
+}
+
+// scalar form (any D, any alignment): one thread per value
+template <typename BT>
+__global__ void merge_n_scalar_kernel(float* acc_out, const float* acc_lse, const __grid_constant__ MergeN m,
+                                      int64_t T, int H, int D, int64_t acc_ls,
+                                      __nv_bfloat16* final_out) {
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= T * H * D) return;
+  const int64_t row = gid / D;
+  const int d = static_cast<int>(gid % D);
+  const int h = static_cast<int>(row / T);
+  const int64_t t = row % T;
+  const int64_t off = (t * H + h) * D + d;
+  const float a = acc_lse[h * acc_ls + t];
+  float mx = a;
+  for (int i = 0; i < m.n; ++i) mx = fmaxf(mx, m.lse[i][h * m.ls[i] + t]);
+  float o = 0.f;
+  if (mx != -INFINITY) {
+    float L = 0.f;
+    if (a != -INFINITY) {
+      L = __expf(a - mx);
+      o = L * acc_out[off];
+    }
+    for (int i = 0; i < m.n; ++i) {
+      const float bi = m.lse[i][h * m.ls[i] + t];
+      if (bi == -INFINITY) continue;
+      const float w = __expf(bi - mx);
+      L += w;
+      o = fmaf(w, static_cast<float>(static_cast<const BT*>(m.blk[i])[off]), o);
+    }
+    o /= L;
+    acc_out[off] = o;
+  }
+  if (final_out) final_out[off] = __float2bfloat16_rn(o);
+}
+
+// the lse update, after the values (they read the old lse)
+__global__ void merge_n_lse_kernel(float* acc_lse, const __grid_constant__ MergeN m, int64_t T, int H,
+                                   int64_t acc_ls) {
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= T * H) return;
+  const int h = static_cast<int>(gid / T);
+  const int64_t t = gid % T;
+  const float a = acc_lse[h * acc_ls + t];
+  float mx = a;
+  for (int i = 0; i < m.n; ++i) mx = fmaxf(mx, m.lse[i][h * m.ls[i] + t]);
+  if (mx == -INFINITY) return;
+  float L = (a == -INFINITY) ? 0.f : __expf(a - mx);
+  for (int i = 0; i < m.n; ++i) {
+    const float bi = m.lse[i][h * m.ls[i] + t];
+    if (bi != -INFINITY) L += __expf(bi - mx);
+  }
+  acc_lse[h * acc_ls + t] = mx + logf(L);
+}
+
+template <typename BT>
+static int merge_n_t(float* acc_out, float* acc_lse, const MergeN& m, int64_t T, int H, int D,
+                     int64_t als, __nv_bfloat16* fin, cudaStream_t s) {
+  bool vec = (D % 8 == 0) && (reinterpret_cast<uintptr_t>(acc_out) % 16 == 0) &&
+             (!fin || reinterpret_cast<uintptr_t>(fin) % 16 == 0);
+  for (int i = 0; i < m.n; ++i) vec = vec && (reinterpret_cast<uintptr_t>(m.blk[i]) % 16 == 0);
+  if (vec) {
+    const int64_t threads = T * H * (D / 8);
+    merge_n_vec8_kernel<BT><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+        acc_out, acc_lse, m, T, H, D, als, fin);
+  } else {
+    const int64_t n = T * H * D;
+    merge_n_scalar_kernel<BT><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+        acc_out, acc_lse, m, T, H, D, als, fin);
+  }
+  merge_n_lse_kernel<<<static_cast<unsigned>((T * H + 255) / 256), 256, 0, s>>>(acc_lse, m, T, H, als);
+  return cuda_status(cudaGetLastError(), "merge_n launch");
+}
+
+int launch_merge_n(float* acc_out, float* acc_lse, int64_t als, const void* const* blk,
+                   int blk_dtype, const float* const* blk_lse, const int64_t* bls, int n,
+                   int64_t T, int H, int D, void* fin, cudaStream_t s) {
+  if (n < 0 || n > TR_MERGE_MAX) return fail(TR_ERR_CONFIG, "merge_n: 0..16 blocks per call");
+  if (T * H * D == 0 || (n == 0 && !fin)) return TR_OK;
+  MergeN m{};
+  m.n = n;
+  for (int i = 0; i < n; ++i) {
+    if (!blk[i] || !blk_lse[i]) return fail(TR_ERR_INPUT, "merge_n: null block");
+    if (bls[i] < T) return fail(TR_ERR_DIMENSION, "merge_n: lse row stride smaller than T");
+    m.blk[i] = blk[i];
+    m.lse[i] = blk_lse[i];
+    m.ls[i] = bls[i];
+  }
+  auto* f = static_cast<__nv_bfloat16*>(fin);
+  if (blk_dtype == TR_DTYPE_BF16) return merge_n_t<__nv_bfloat16>(acc_out, acc_lse, m, T, H, D, als, f, s);
+  if (blk_dtype == TR_DTYPE_F32) return merge_n_t<float>(acc_out, acc_lse, m, T, H, D, als, f, s);
+  return fail(TR_ERR_INPUT, "unknown blk dtype");
+}
+
 __global__ void fill_kernel(float* p, int64_t n, float v) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;

@@ -174,6 +174,41 @@ def merge_state_(acc_out, acc_lse, blk_out, blk_lse, final_out=None):
     return acc_out, acc_lse
 
 
+def merge_n_(acc_out, acc_lse, blocks, final_out=None):
+    """In place: acc <- merge(acc, *blocks) in one pass per TR_MERGE_MAX
+    blocks (tr_merge_n).  ``blocks``: [(blk_out, blk_lse)], blk_out bf16 or
+    float32 (T,H,D) contiguous (all the same dtype), blk_lse float32 (H, T)
+    with unit column stride (column slices of wider buffers are fine)."""
+    _require_cuda("acc_out", acc_out, torch.float32)
+    t, h, d = acc_out.shape
+    if acc_lse.dtype != torch.float32 or acc_lse.shape != (h, t) or acc_lse.stride(1) != 1:
+        raise DimensionError("acc_lse must be float32 (H, T) with unit column stride")
+    dtypes = {bo.dtype for bo, _ in blocks}
+    if len(dtypes) > 1 or not dtypes <= {torch.bfloat16, torch.float32}:
+        raise DimensionError("blocks must all be bf16 or all float32")
+    for bo, bl in blocks:
+        if not bo.is_cuda or not bo.is_contiguous() or bo.shape != acc_out.shape:
+            raise DimensionError(f"block of shape {tuple(bo.shape)} does not match the "
+                                 f"accumulator {tuple(acc_out.shape)}")
+        if bl.dtype != torch.float32 or bl.shape != (h, t) or bl.stride(1) != 1:
+            raise DimensionError("block lse must be float32 (H, T) with unit column stride")
+    if final_out is not None:
+        _require_cuda("final_out", final_out, torch.bfloat16)
+    dt = _lib.TR_DTYPE_F32 if dtypes == {torch.float32} else _lib.TR_DTYPE_BF16
+    groups = [blocks[i:i + _lib.TR_MERGE_MAX] for i in range(0, len(blocks), _lib.TR_MERGE_MAX)]
+    for gi, grp in enumerate(groups or [[]]):
+        n = len(grp)
+        outs = (ctypes.c_void_p * max(1, n))(*[bo.data_ptr() for bo, _ in grp])
+        lses = (ctypes.c_void_p * max(1, n))(*[bl.data_ptr() for _, bl in grp])
+        strides = (ctypes.c_int64 * max(1, n))(*[bl.stride(0) for _, bl in grp])
+        fin = _ptr(final_out) if final_out is not None and gi == len(groups or [[]]) - 1 else None
+        _lib.check(_lib.lib().tr_merge_n(
+            _ptr(acc_out), _ptr(acc_lse), acc_lse.stride(0), outs, dt, lses, strides, n, t, h, d,
+            fin, _stream(acc_out.device)))
+        _count(2)
+    return acc_out, acc_lse
+
+
 def merge_state(acc_out, acc_lse, blk_out, blk_lse):
     out = acc_out.to(torch.float32, copy=True).contiguous()
     lse = acc_lse.to(torch.float32, copy=True).contiguous()

@@ -53,6 +53,9 @@ class CudaOps:
     def merge_(self, acc_out, acc_lse, blk_out, blk_lse):
         kernels.merge_state_(acc_out, acc_lse, blk_out, blk_lse)
 
+    def merge_n_(self, acc_out, acc_lse, blocks):
+        kernels.merge_n_(acc_out, acc_lse, blocks)
+
     def init_(self, acc_out, acc_lse):
         kernels.partial_init_(acc_out, acc_lse)
 
@@ -136,24 +139,28 @@ class FusedPlan:
 
     push[s] = (msg, dst, row0, row1): computing step s writes its rows
         [row0, row1) of the traveling-Q layout (all of them, in layout order)
-        straight into ``dst``'s receive slot msg % 2 -- the OUT_LSE message the
-        reference sends at step msg = s + 1 (engine.py:346-353).
-    recv[k] = (src, ids, slot): message k arrives in my slot k % 2; it is
-        merged at the start of step k + 1 (after the loop for the final phase),
-        as engine.py:187-200 wires the MergePlan.
-    grant_at_start: [(src, k)] -- the first message into each slot: its sender
-        may push as soon as the call starts.
-    grant_after[k] = (src, k2): after merging message k, slot k % 2 is free for
-        message k2 from src.
+        straight into ``dst``'s receive slot for message msg -- the OUT_LSE
+        message the reference sends at step msg = s + 1 (engine.py:346-353).
+    recv[k] = (src, ids, slot): message k arrives in my slot ``slot`` (one
+        slot per message, in step order, never reused within a forward);
+        all of them are folded into the accumulator by ONE n-way merge per
+        home chunk after the last step -- the MergePlans of engine.py:187-200
+        and 620-628 applied at once (the merge is associative).
     """
     push: dict
     recv: dict
-    grant_at_start: list
-    grant_after: dict
+
+    def slot_of(self, k):
+        return self.recv[k][2]
+
+    def merge_groups(self, home_ids):
+        """For each home chunk: [(slot, position of the chunk in the message)]."""
+        return {a: [(slot, ids.index(a)) for _, (_, ids, slot) in sorted(self.recv.items())
+                    if a in ids] for a in home_ids}
 
 
 def fused_plan(prog, c) -> FusedPlan:
-    """Derive the push/merge/grant program of one rank from its step program
+    """Derive the push / receive program of one rank from its step program
     (``compile_rank``); ScheduleError if a message is not a whole step's
     rows (never the case for the reference's token-ring schedules)."""
     push, recv = {}, {}
@@ -170,17 +177,8 @@ def fused_plan(prog, c) -> FusedPlan:
             if len(st.recv_out) != 1:
                 raise ScheduleError(f"step {k}: more than one return per step")
             src, ids = st.recv_out[0]
-            recv[k] = (src, tuple(ids), k % 2)
-    order = sorted(recv)
-    grant_at_start, grant_after, last_in_slot = [], {}, {}
-    for k in order:
-        src, _, slot = recv[k]
-        if slot in last_in_slot:
-            grant_after[last_in_slot[slot]] = (src, k)
-        else:
-            grant_at_start.append((src, k))
-        last_in_slot[slot] = k
-    return FusedPlan(push, recv, grant_at_start, grant_after)
+            recv[k] = (src, tuple(ids), len(recv))
+    return FusedPlan(push, recv)
 
 
 class TokenRingAttention:
@@ -224,7 +222,13 @@ class TokenRingAttention:
         if transport not in TRANSPORTS:
             raise ConfigError(f"transport must be one of {TRANSPORTS}, got {transport!r}")
         self.transport = transport if self.P > 1 else "nccl"
-        self.fplan = fused_plan(self.prog, self.c) if self.transport == "fused" else None
+        self.fplan = self.fplans = None
+        if self.transport == "fused":
+            # every rank's plan: a sender needs the slot index its message
+            # has at the home
+            self.fplans = {r: fused_plan(compile_rank(self.sched, r) if r != self.rank
+                                         else self.prog, self.c) for r in range(self.P)}
+            self.fplan = self.fplans[self.rank]
         self._alloc()
         if self.transport in ("ipc", "fused"):
             self._ipc_setup()
@@ -236,15 +240,20 @@ class TokenRingAttention:
         self.obuf = [torch.empty((rows, H, D), dtype=bf, device=dev) for _ in range(2)]
         self.lbuf = [torch.empty((H, rows), dtype=torch.float32, device=dev) for _ in range(2)]
         self.lse_send = torch.empty((H, rows), dtype=torch.float32, device=dev)
-        self.out_recv = torch.empty((rows, H, D), dtype=bf, device=dev)
-        self.lse_recv = torch.empty((H, rows), dtype=torch.float32, device=dev)
+        recv_rows = rows if self.transport != "fused" else 1     # fused: per-message slots
+        self.out_recv = torch.empty((recv_rows, H, D), dtype=bf, device=dev)
+        self.lse_recv = torch.empty((H, recv_rows), dtype=torch.float32, device=dev)
         self.acc_out = torch.empty((rows, H, D), dtype=torch.float32, device=dev)
         self.acc_lse = torch.empty((H, rows), dtype=torch.float32, device=dev)
+        self.slots = []
         if self.transport == "fused":
-            # second receive slot (messages alternate slots by step parity) and
-            # the launch counter the pushing kernels use for their done flag
-            self.out_recv2 = torch.empty((rows, H, D), dtype=bf, device=dev)
-            self.lse_recv2 = torch.empty((H, rows), dtype=torch.float32, device=dev)
+            # one receive slot per message of a forward (bf16 rows + lse), all
+            # folded by one n-way merge at the end; and the launch counter the
+            # pushing kernels use for their done flag
+            for k, (_, ids, _) in sorted(self.fplan.recv.items()):
+                n = len(ids) * self.c
+                self.slots.append((torch.empty((n, H, D), dtype=bf, device=dev),
+                                   torch.empty((H, n), dtype=torch.float32, device=dev)))
             self.done_count = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # -- transport -----------------------------------------------------------
@@ -277,16 +286,15 @@ class TokenRingAttention:
     #   flags[4+s] q_ready from s: highest step whose Q from rank s has landed
     #              (one per source: the direct route has two Q senders per step)
     # fused transport (OUT pushed by the attention epilogue) adds
-    #   flags[4+P+s]   o_ready of receive slot s (raised by the pushing kernel)
-    #   flags[6+P+k]   push grant for message k (raised by its home, once the
-    #                  slot the message lands in has been merged)
+    #   flags[4+P+s]   o_ready of receive slot s (raised by the pushing kernel's
+    #                  last CTA); slot s's buffers are shared as entries 5+2s, 6+2s
     def _ipc_setup(self):
         from torch.multiprocessing.reductions import reduce_tensor
-        self.flags = torch.zeros(4 + self.P + 2 + len(self.prog) + 1, dtype=torch.int64,
+        self.flags = torch.zeros(4 + self.P + len(self.prog) + 1, dtype=torch.int64,
                                  device=self.device)
         shared = [self.qbuf[0], self.qbuf[1], self.out_recv, self.lse_recv, self.flags]
-        if self.transport == "fused":
-            shared += [self.out_recv2, self.lse_recv2]
+        for o, l in self.slots:
+            shared += [o, l]
         mine = [reduce_tensor(t) for t in shared]
         everyone = [None] * self.P
         dist.all_gather_object(everyone, mine, group=self.group)
@@ -309,11 +317,10 @@ class TokenRingAttention:
         return self.flags if r == self.rank else self.peer[r][4]
 
     def _recv_slot(self, slot, r=None):
-        """(out, lse) receive buffers of slot 0/1 -- mine, or peer r's."""
+        """(out, lse) of fused receive slot ``slot`` -- mine, or peer r's."""
         if r is None or r == self.rank:
-            return (self.out_recv, self.lse_recv) if slot == 0 else (self.out_recv2, self.lse_recv2)
-        p = self.peer[r]
-        return (p[2], p[3]) if slot == 0 else (p[5], p[6])
+            return self.slots[slot]
+        return self.peer[r][5 + 2 * slot], self.peer[r][6 + 2 * slot]
 
     @contextlib.contextmanager
     def _timed_copy(self, ev, key, stream, nbytes):
@@ -330,7 +337,7 @@ class TokenRingAttention:
     def _forward_ipc(self, q_loc, k_loc, v_loc) -> Partial:
         c, rank, P, H = self.c, self.rank, self.P, self.H
         fused, fp = self.transport == "fused", self.fplan
-        O0, G0 = 4 + P, 6 + P          # fused: o_ready slots, push grants
+        O0 = 4 + P                     # fused: o_ready flag of each receive slot
         base = self.calls * (P + 4) + 8
         self.calls += 1
         cur = torch.cuda.current_stream(self.device)
@@ -340,9 +347,6 @@ class TokenRingAttention:
         self.flags[4:] = base - 1
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self.group)
-        if fused:
-            for src, k in fp.grant_at_start:      # my empty slots: their first messages may go
-                kernels.flag_set_(self._flags_of(src)[G0 + k:G0 + k + 1], base + k, cur)
         if not self.direct_first:
             self.ops.init_(self.acc_out, self.acc_lse)
         local_layout = self.prog[0].q_layout
@@ -357,24 +361,18 @@ class TokenRingAttention:
             if i >= 1 and (st.q_ids or st.send_q):
                 for src, _ in self.prog[i - 1].recv_q:                  # Q_i has landed
                     kernels.flag_wait_(self.flags[4 + src:5 + src], base + i, cur)
-            if i >= 1 and self.prog[i - 1].recv_out:
-                o = O0 + (i - 1) % 2 if fused else 2
-                kernels.flag_wait_(self.flags[o:o + 1], base + i - 1, cur)
+            if i >= 1 and self.prog[i - 1].recv_out and not fused:
+                kernels.flag_wait_(self.flags[2:3], base + i - 1, cur)
             if self.record_timeline:
                 ev["comm_ready"] = self.ops.event()
                 self.ops.record(ev["comm_ready"])
-            if i >= 1 and self.prog[i - 1].recv_out:
+            if i >= 1 and self.prog[i - 1].recv_out and not fused:
                 # OUT sent to me at step i-1 has landed: merge it, free the buffer
                 src, ids = self.prog[i - 1].recv_out[0]
                 n = len(ids) * c
-                ob, lb = self._recv_slot((i - 1) % 2 if fused else 0)
-                self._merge_returned((ids, ob[:n], lb.view(-1)[: H * n].view(H, n)),
-                                     local_layout)
-                if not fused:
-                    kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
-                elif (i - 1) in fp.grant_after:   # slot free: grant the next message into it
-                    s2, k2 = fp.grant_after[i - 1]
-                    kernels.flag_set_(self._flags_of(s2)[G0 + k2:G0 + k2 + 1], base + k2, cur)
+                self._merge_returned((ids, self.out_recv[:n],
+                                      self.lse_recv.view(-1)[: H * n].view(H, n)), local_layout)
+                kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
             cur_q = self.qbuf[i % 2] if i > 0 else q_loc
             ev_q = torch.cuda.Event()
             ev_q.record(cur)
@@ -411,18 +409,6 @@ class TokenRingAttention:
                 kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
                             self.sched.chunks[b].start) for b in st.kv_ids]
                 buf = i % 2
-                if fused and i in fp.push:
-                    # the home's grant for my push (it has merged the previous
-                    # message in that slot) -- after my own merge above, so the
-                    # ranks never wait on each other in a cycle
-                    k = fp.push[i][0]
-                    if self.record_timeline:
-                        ev["grant_wait"] = self.ops.event()
-                        self.ops.record(ev["grant_wait"])
-                    kernels.flag_wait_(self.flags[G0 + k:G0 + k + 1], base + k, cur)
-                    if self.record_timeline:
-                        ev["granted"] = self.ops.event()
-                        self.ops.record(ev["granted"])
                 if self.record_timeline:
                     ev["attn_start"] = self.ops.event()
                     self.ops.record(ev["attn_start"])
@@ -433,15 +419,16 @@ class TokenRingAttention:
                     # compute + send in one kernel: rows go straight into the
                     # home's receive slot over NVLink; its last CTA raises the
                     # home's o_ready flag
+                    # (the slot holds only message k, and the previous call's
+                    # merge of it finished before this call's barrier)
                     k, dst, a, b = fp.push[i]
-                    ob, lb = self._recv_slot(k % 2, dst)
-                    n = b - a
-                    ev["o_push_bytes"] = n * H * (2 * self.D + 4)   # carried by this launch
-                    o = O0 + k % 2
+                    slot = self.fplans[dst].slot_of(k)
+                    ob, lb = self._recv_slot(slot, dst)
+                    ev["o_push_bytes"] = (b - a) * H * (2 * self.D + 4)   # carried by this launch
+                    o = O0 + slot
                     kernels.attention_segments_push(
-                        cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal, ob[:n],
-                        lb.view(-1)[: H * n].view(H, n), a, self.done_count,
-                        self._flags_of(dst)[o:o + 1], base + k)
+                        cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal, ob, lb, a,
+                        self.done_count, self._flags_of(dst)[o:o + 1], base + k)
                 else:
                     self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
                                        self.obuf[buf], self.lbuf[buf])
@@ -467,15 +454,39 @@ class TokenRingAttention:
                 cs.wait_event(ev_comp[i])
                 kernels.flag_set_(self.flags[1:2], base + i, cs)
         last = self.prog[-1]
-        if last.recv_out:
-            o = O0 + last.step % 2 if fused else 2
-            kernels.flag_wait_(self.flags[o:o + 1], base + last.step, cur)
+        if fused:
+            self._merge_all_fused(base, cur, local_layout)
+        elif last.recv_out:
+            kernels.flag_wait_(self.flags[2:3], base + last.step, cur)
             src, ids = last.recv_out[0]
             n = len(ids) * c
-            ob, lb = self._recv_slot(last.step % 2 if fused else 0)
-            self._merge_returned((ids, ob[:n], lb.view(-1)[: H * n].view(H, n)), local_layout)
+            self._merge_returned((ids, self.out_recv[:n],
+                                  self.lse_recv.view(-1)[: H * n].view(H, n)), local_layout)
         cur.wait_stream(cs)
         return Partial(self.acc_out, self.acc_lse)
+
+    def _merge_all_fused(self, base, cur, local_layout):
+        """Wait for every pushed message, then fold all of them into the
+        accumulator: one n-way merge per home chunk (tr_merge_n)."""
+        fp, c, P = self.fplan, self.c, self.P
+        ev = {}
+        if self.record_timeline:
+            ev["start"] = self.ops.event()
+            self.ops.record(ev["start"])
+        for k, (_, _, slot) in sorted(fp.recv.items()):
+            kernels.flag_wait_(self.flags[4 + P + slot:5 + P + slot], base + k, cur)
+        if self.record_timeline:
+            ev["comm_ready"] = self.ops.event()
+            self.ops.record(ev["comm_ready"])
+            self.timeline.append(ev)
+        for a, parts in fp.merge_groups(local_layout).items():
+            if self.sched.chunks[a].home != self.rank:
+                raise ScheduleError(f"rank {self.rank}: chunk {a} homes elsewhere")
+            l0 = self.part.local_offset(self.rank, self.sched.chunks[a].start)
+            blocks = [(self.slots[slot][0][j * c:(j + 1) * c],
+                       self.slots[slot][1][:, j * c:(j + 1) * c]) for slot, j in parts]
+            if blocks:
+                self.ops.merge_n_(self.acc_out[l0:l0 + c], self.acc_lse[:, l0:l0 + c], blocks)
 
     def __call__(self, q_loc, k_loc, v_loc) -> Partial:
         if self.transport in ("ipc", "fused"):

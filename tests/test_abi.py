@@ -31,7 +31,7 @@ def lib():
 def test_header_declares_expected_api():
     fns = declared_functions()
     assert fns == sorted(["tr_attention_block", "tr_attention_segments",
-                          "tr_attention_segments_push", "tr_merge_state",
+                          "tr_attention_segments_push", "tr_merge_state", "tr_merge_n",
                           "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
                           "tr_copy_async", "tr_enable_peer_access", "tr_version",
                           "tr_kernel_count", "tr_last_error"])

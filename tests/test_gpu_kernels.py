@@ -221,3 +221,43 @@ def test_merge_identity_exact(K):
     assert torch.equal(o, blk.float()) and torch.equal(l, bl)
     o2, l2 = K.merge_state(o, l, torch.zeros_like(blk), al)
     assert torch.equal(o2, o) and torch.equal(l2, l)
+
+
+@pytest.mark.parametrize("d,n,dtype", [(128, 7, torch.bfloat16), (64, 3, torch.float32),
+                                       (128, 20, torch.bfloat16), (12, 4, torch.bfloat16),
+                                       (128, 0, torch.bfloat16)])
+def test_merge_n_vs_sequential_oracle(K, d, n, dtype):
+    """tr_merge_n folds n partials at once; the oracle folds them one merge_state
+    (ref _kernels.pyx:68-102) at a time.  Rows where the accumulator, some
+    blocks, or everything is -inf exercise the identities; n=20 chains two
+    calls (TR_MERGE_MAX=16); d=12 takes the scalar kernel; lse blocks are
+    column slices of wider arrays (row stride != T)."""
+    t, h = 96, 3
+    g = torch.Generator().manual_seed(d * 100 + n)
+    acc = torch.randn(t, h, d, generator=g)
+    al = torch.randn(h, t, generator=g) * 3
+    al[:, :5] = -float("inf")
+    acc[:5] = 0.0
+    blocks, ref_o, ref_l = [], acc.double().numpy(), al.double().numpy()
+    for i in range(n):
+        bo = torch.randn(t, h, d, generator=g).to(dtype)
+        wide = torch.randn(h, t + 17, generator=g) * 3
+        bl = wide[:, 7:7 + t]
+        bl[:, (3 * i) % t] = -float("inf")        # a dead row per block
+        bl[:, :2] = -float("inf")                 # rows 0-1: everything dead
+        if i == 0:
+            bl[:, 2:5] = wide[:, 9:12]            # rows 2-4: only blocks contribute
+        blocks.append((bo.cuda(), wide.cuda()[:, 7:7 + t]))
+        ref_o, ref_l = ok.merge_state(ref_o, ref_l, bo.double().numpy(), bl.double().numpy())
+    acc_d, al_d = acc.cuda(), al.cuda()
+    fin = torch.empty(t, h, d, dtype=torch.bfloat16, device="cuda")
+    K.merge_n_(acc_d, al_d, blocks, final_out=fin)
+    torch.cuda.synchronize()
+    lse = al_d.double().cpu().numpy()
+    out = acc_d.double().cpu().numpy()
+    fin_ok = np.isfinite(ref_l)
+    assert np.array_equal(np.isfinite(lse), fin_ok)
+    assert np.abs(lse[fin_ok] - ref_l[fin_ok]).max() <= 5e-5
+    assert np.abs(out - ref_o).max() <= 5e-5
+    assert np.all(out[:2] == 0.0)
+    assert torch.equal(fin, acc_d.to(torch.bfloat16))
