@@ -196,10 +196,12 @@ __global__ void __launch_bounds__(256) merge_n_vec8_kernel(float* __restrict__ a
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = 0.f;
   }
+  // (batching the block loads ahead of the math measured slower: 72 vs 42
+  // registers, 0.241 vs 0.200 ms for c=8192, H=32, n=7)
 #pragma unroll
   for (int i = 0; i < TR_MERGE_MAX; ++i) {
     if (i >= m.n) break;
-    if (b[i] == -INFINITY) continue;
+    if (b[i] == -INFINITY) continue;      // exact identity: its values are never read
     const float w = __expf(b[i] - mx);
     L += w;
     float x[8];

@@ -81,3 +81,56 @@ def test_token_ring_ipc(world, S, H, D, causal, route, transport):
         fin = np.isfinite(ref[r][1])
         assert np.array_equal(np.isfinite(res[r][1]), fin)
         assert np.abs(res[r][1][fin] - ref[r][1][fin]).max() <= 1e-3
+
+
+def _worker_full(rank, world, port, S, H, D, q_out):
+    """Full-size fused forward; compares this rank's rows with one dense causal
+    launch of the same inputs (computed in-process on this rank's rows)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2412_20501_b200 as tr
+        from paper_2412_20501_b200.ring import TokenRingAttention
+        runner = TokenRingAttention(S, H, D, causal=True, device=torch.device("cuda", 0),
+                                    transport="fused")
+        q, k, v = tr.rng.local_inputs(4, runner.part, rank, H, D)
+        for _ in range(2):
+            res = runner(q, k, v)
+        torch.cuda.synchronize()
+        fq, fk, fv = tr.rng.attention_inputs(4, S, H, D, device="cuda")
+        worst_o = worst_l = 0.0
+        for lo, hi in runner.part.ranges(rank):
+            # dense rows [lo, hi) against keys [0, hi): the causal block at q_offset lo
+            do, dl = tr.kernels.attention_block(fq[lo:hi].contiguous(), fk[:hi].contiguous(),
+                                                fv[:hi].contiguous(), 2, lo, 0)
+            l0 = runner.part.local_offset(rank, lo)
+            n = hi - lo
+            worst_o = max(worst_o, (res.out[l0:l0 + n] - do.float()).abs().max().item())
+            worst_l = max(worst_l, (res.lse[:, l0:l0 + n] - dl).abs().max().item())
+        q_out.put((rank, worst_o, worst_l))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_full_size_vs_dense_launch(world):
+    """Config-3 sequence length (S=131072, D=128; H=4 to bound the time)
+    through the fused transport with `world` processes on one GPU: every rank's
+    home rows equal one dense causal launch within the bf16 tolerance."""
+    S, H, D = 131072, 4, 128
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_full, args=(r, world, port, S, H, D, q_out))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q_out.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for r, wo, wl in got:
+        assert wo <= 2e-2 and wl <= 1e-3, (r, wo, wl)
