@@ -48,6 +48,13 @@ struct AttnCfg {
 #define TR_POLY_MOD 6
 #endif
   static constexpr int POLY_MOD = TR_POLY_MOD;   // 1 of every POLY_MOD exp2 pairs on the FMA pipe
+#ifndef TR_P_CHUNKS
+#define TR_P_CHUNKS 2
+#endif
+  // P is published to the MMA warp in NPC key chunks (each its own barrier),
+  // so O += P.V starts on the first chunk while the rest is still exponentiated
+  static constexpr int NPC = TR_P_CHUNKS;
+  static_assert(NPC == 2 || NPC == 4, "P chunks: 2 or 4");
 };
 
 // Per-CTA kv tile walk: the tile count of every kv segment lives in shared
@@ -102,16 +109,18 @@ __device__ __forceinline__ void q_tile_of(const AttnPlan& p, int64_t lin, int& s
 }
 
 // exp2 of one S row (already in registers) -> bf16 P in TMEM, row sums in
-// packed accumulators; arrives on pbar[kh] after each 64-key half.
-template <int POLY_MOD, bool kPoly>
+// packed accumulators; arrives on pbar[kh] after each of the NPC key chunks.
+template <int POLY_MOD, bool kPoly, int NPC>
 __device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, uint64_t c2,
                                        uint64_t nmc2, uint64_t (&lsum2)[2], uint64_t* pbar) {
+  constexpr int PAIRS = 64 / NPC;        // bf16 pairs (= TMEM columns) per chunk
   #pragma unroll
-  for (int kh = 0; kh < 2; ++kh) {
-    uint32_t pk[32];
+  for (int kh = 0; kh < NPC; ++kh) {
+    uint32_t pk[PAIRS];
     #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int e = kh * 64 + 2 * i;
+    for (int ii = 0; ii < PAIRS; ++ii) {
+      const int i = kh * PAIRS + ii;     // pair index in the row
+      const int e = 2 * i;
       const uint64_t x2 = ffma2(f2pack(__uint_as_float(s[e]), __uint_as_float(s[e + 1])), c2, nmc2);
       float a, b;
       f2unpack(x2, a, b);
@@ -123,9 +132,10 @@ __device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, ui
       lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
       float pa, pb;
       f2unpack(p2, pa, pb);
-      pk[i] = pack_bf16x2(pa, pb);
+      pk[ii] = pack_bf16x2(pa, pb);
     }
-    tmem_st32(tS + kh * 32, pk);
+    if constexpr (PAIRS == 32) tmem_st32(tS + kh * 32, pk);
+    else tmem_st16(tS + kh * 16, pk);
     tc_wait_st();
     tc_fence_before();
     mbar_arrive(&pbar[kh]);
@@ -146,10 +156,10 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   uint64_t* kv_full = bars + 1;                 // [NS]
   uint64_t* kv_empty = bars + 1 + C::NS;        // [NS]
   uint64_t* s_full = bars + 1 + 2 * C::NS;      // [2]
-  uint64_t* p_full = bars + 3 + 2 * C::NS;      // [2 halves][2 key halves]
-  uint64_t* o_done = bars + 7 + 2 * C::NS;      // [2]
-  int64_t* kv_tiles = reinterpret_cast<int64_t*>(bars + 9 + 2 * C::NS);  // [4]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 2 * C::NS);
+  uint64_t* p_full = bars + 3 + 2 * C::NS;      // [2 halves][NPC key chunks]
+  uint64_t* o_done = p_full + 2 * C::NPC;       // [2]
+  int64_t* kv_tiles = reinterpret_cast<int64_t*>(o_done + 2);  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 6);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -166,8 +176,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
     for (int h = 0; h < 2; ++h) {
       mbar_init(&s_full[h], 1);
-      mbar_init(&p_full[2 * h], 128);
-      mbar_init(&p_full[2 * h + 1], 128);
+      for (int kh = 0; kh < C::NPC; ++kh) mbar_init(&p_full[C::NPC * h + kh], 128);
       mbar_init(&o_done[h], 1);
     }
     fence_barrier_init();
@@ -244,23 +253,24 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         mma_ss_elect(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
       }
     };
-    // O_h += P_h[:, keys of half kh] . V[keys of half kh, :]
+    // O_h += P_h[:, keys of chunk kh] . V[keys of chunk kh, :]
+    constexpr int KPC = 8 / C::NPC;      // 16-key MMA steps per P chunk
     auto pv = [&](int h, int stage, int kh, bool acc) {
       const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
       #pragma unroll
-      for (int k4 = 0; k4 < 4; ++k4) {
-        const int kk = kh * 4 + k4;
+      for (int k4 = 0; k4 < KPC; ++k4) {
+        const int kk = kh * KPC + k4;
         mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
                      C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
       }
     };
     auto pv_both = [&](int h, int stage, uint32_t phase, bool acc) {
-      mbar_wait(&p_full[2 * h], phase);
-      tc_fence_after();
-      pv(h, stage, 0, acc);
-      mbar_wait(&p_full[2 * h + 1], phase);
-      tc_fence_after();
-      pv(h, stage, 1, true);
+      #pragma unroll
+      for (int kh = 0; kh < C::NPC; ++kh) {
+        mbar_wait(&p_full[C::NPC * h + kh], phase);
+        tc_fence_after();
+        pv(h, stage, kh, acc || kh > 0);
+      }
     };
     int prev_v_stage = 0;
     int sk = 0;
@@ -321,8 +331,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
 #ifdef TR_EXP_NOSOFTMAX
       // experiment: measure the MMA/TMA pipeline alone (results are garbage)
       tc_fence_before();
-      mbar_arrive(&p_full[2 * h]);
-      mbar_arrive(&p_full[2 * h + 1]);
+      for (int kh = 0; kh < C::NPC; ++kh) mbar_arrive(&p_full[C::NPC * h + kh]);
       continue;
 #endif
       uint32_t s[128];
@@ -340,6 +349,19 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         #pragma unroll
         for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;  // -inf
       }
+#if defined(TR_MAX_CHAINS) && TR_MAX_CHAINS == 4
+      // four independent 3-input max chains (16 deep instead of 32)
+      float m4[4];
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) m4[u] = fmaxf(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1]));
+      #pragma unroll
+      for (int i = 8; i < 128; i += 8) {
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+          m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
+      }
+      float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+#else
       float mx = __uint_as_float(s[0]);
       float mxb = __uint_as_float(s[1]);
       #pragma unroll
@@ -348,6 +370,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
       }
       mx = fmaxf(mx, mxb);
+#endif
       TR_TRACE_AT(2, j);
       const bool grow = mx > m_used + thresh;
       const bool scale_o = grow && m_used != -INFINITY;
@@ -381,9 +404,9 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       // tiles keep every exp2 on MUFU (exact 0 for -inf); full tiles move one
       // pair in POLY_MOD to the FMA pipe.
       if (need_mask)
-        emit_p<C::POLY_MOD, false>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
+        emit_p<C::POLY_MOD, false, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
       else
-        emit_p<C::POLY_MOD, true>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
+        emit_p<C::POLY_MOD, true, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
       TR_TRACE_AT(3, j);
     }
     float l;
