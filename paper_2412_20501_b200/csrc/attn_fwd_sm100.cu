@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "tr_internal.h"
@@ -108,6 +109,35 @@ __device__ __forceinline__ void q_tile_of(const AttnPlan& p, int64_t lin, int& s
   row0 = local * 256;
 }
 
+// This CTA's (head, q segment, first row): the explicit longest-first order
+// when the host supplied one, else head-major with q_tile_of's order.
+__device__ __forceinline__ void cta_tile(const AttnPlan& p, int64_t item, int& head, int& seg,
+                                         int64_t& row0) {
+  const int64_t nt = p.tile_prefix[p.nq];
+  if (p.n_order == 0) {
+    head = static_cast<int>(item / nt);
+    q_tile_of(p, item % nt, seg, row0);
+    return;
+  }
+  const int64_t G = p.head_group;
+  const int64_t full = p.heads / G;          // complete head groups
+  int64_t idx = item, g, hg;
+  if (idx < full * G * nt) {
+    g = idx / (G * nt);
+    idx -= g * G * nt;
+    hg = G;
+  } else {
+    g = full;
+    idx -= full * G * nt;
+    hg = p.heads - full * G;
+  }
+  head = static_cast<int>(g * G + idx % hg);
+  int64_t lin = p.order[idx / hg];
+  seg = 0;
+  while (seg + 1 < p.nq && lin >= p.tile_prefix[seg + 1]) ++seg;
+  row0 = (lin - p.tile_prefix[seg]) * 256;
+}
+
 // exp2 of one S row (already in registers) -> bf16 P in TMEM, row sums in
 // packed accumulators; arrives on pbar[kh] after each of the NPC key chunks.
 template <int POLY_MOD, bool kPoly, int NPC>
@@ -163,11 +193,10 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int head = static_cast<int>(blockIdx.x / p.tile_prefix[p.nq]);
-  const int64_t lin = blockIdx.x % p.tile_prefix[p.nq];
+  int head;
   int qseg;
   int64_t qrow0;  // first row of this CTA inside its q segment
-  q_tile_of(p, lin, qseg, qrow0);
+  cta_tile(p, blockIdx.x, head, qseg, qrow0);
   const tr_segment Q = p.q[qseg];
   const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
 
@@ -462,6 +491,352 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   }
   tc_fence_before();
   if (p.done_flag) __threadfence_system();   // out/lse rows may live on a peer GPU
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+  if (p.done_flag && threadIdx.x == 0) signal_done(p);
+}
+
+// ============================================================================
+// Persistent form of attn_fwd_sm100_kernel: one CTA per SM walks the work
+// items (head x 256-row q tile, in the same order as the one-CTA-per-item
+// grid) with a static stride of gridDim.x.  Barrier initialisation, the TMEM
+// allocation and the tensor-map prefetch happen once per SM instead of once
+// per item, and consecutive items overlap: the producer loads the next
+// item's Q (as soon as the last QK of the current item has read the Q tile)
+// and K/V into the ring while the current item drains, the next item's first
+// QK MMAs run while the softmax warps are still in the current item's
+// epilogue, and the epilogue releases O right after reading it (o_free) so
+// the next P.V can overwrite it.  Every barrier phase is tracked across
+// items: per-tile barriers by a running tile count, per-item barriers by a
+// running count of items that have kv tiles.
+template <int D>
+__device__ __forceinline__ int item_kv_tiles(const AttnPlan& p, int64_t qmax_pos, int lane,
+                                             int64_t* my_tiles) {
+  // this warp's copy of the item's per-kv-segment tile counts
+  if (lane < TR_MAX_SEGMENTS) {
+    int64_t n = 0;
+    if (lane < p.nkv) {
+      n = (p.kv[lane].rows + 127) / 128;
+      if (p.causal)
+        n = (qmax_pos < p.kv[lane].pos0) ? 0 : imin64(n, (qmax_pos - p.kv[lane].pos0) / 128 + 1);
+    }
+    my_tiles[lane] = n;
+  }
+  __syncwarp();
+  return __shfl_sync(0xffffffffu,
+                     static_cast<int>(my_tiles[0] + my_tiles[1] + my_tiles[2] + my_tiles[3]), 0);
+}
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+attn_fwd_persistent_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+                           const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnPlan p) {
+  using C = AttnCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                      // 2 tiles
+  uint8_t* sKV = smem + 2 * C::TILE;       // NS tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_TILES);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;                 // [NS]
+  uint64_t* kv_empty = kv_full + C::NS;         // [NS]
+  uint64_t* s_full = kv_empty + C::NS;          // [2]
+  uint64_t* p_full = s_full + 2;                // [2 halves][NPC key chunks]
+  uint64_t* o_done = p_full + 2 * C::NPC;       // [2]
+  uint64_t* o_free = o_done + 2;                // [2]
+  int64_t* kv_tiles = reinterpret_cast<int64_t*>(o_free + 2);   // [12 warps][4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_tiles + 12 * 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  int64_t* my_tiles = kv_tiles + warp * 4;
+  const int64_t n_items = p.tile_prefix[p.nq] * p.heads;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&s_full[h], 1);
+      for (int kh = 0; kh < C::NPC; ++kh) mbar_init(&p_full[C::NPC * h + kh], 128);
+      mbar_init(&o_done[h], 1);
+      mbar_init(&o_free[h], 128);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmq); tma_prefetch_desc(&tmk); tma_prefetch_desc(&tmv);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp < 4) {
+   setmaxnreg_dec<56>();
+   if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    int s = 0;
+    uint32_t round = 0, act = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      int head, qseg;
+      int64_t qrow0;
+      cta_tile(p, item, head, qseg, qrow0);
+      const tr_segment Q = p.q[qseg];
+      const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
+      const int ntiles = item_kv_tiles<D>(p, qmax_pos, lane, my_tiles);
+      if (ntiles == 0) continue;
+      const int32_t col0 = head * D;
+      mbar_wait(q_empty, (act & 1) ^ 1);     // the previous item's QKs have read sQ
+      mbar_arrive_expect_tx_elect(q_full, 2 * C::TILE);
+      for (int h = 0; h < 2; ++h)
+        for (int b = 0; b < C::NB; ++b)
+          tma_load_2d_elect(sQ + (h * C::NB + b) * C::BOX, &tmq, q_full, col0 + 64 * b,
+                            static_cast<int32_t>(Q.row0 + qrow0 + 128 * h), kEvictFirst);
+      KvWalk w = kv_begin(my_tiles);
+      for (int j = 0; j < ntiles; ++j, w.next(my_tiles)) {
+        const int32_t krow = static_cast<int32_t>(p.kv[w.g].row0 + w.t * 128);
+        #pragma unroll
+        for (int which = 0; which < 2; ++which) {
+          mbar_wait(&kv_empty[s], (round & 1) ^ 1);
+          mbar_arrive_expect_tx_elect(&kv_full[s], C::TILE);
+          const CUtensorMap* tm = which ? &tmv : &tmk;
+          #pragma unroll
+          for (int b = 0; b < C::NB; ++b)
+            tma_load_2d_elect(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b, krow,
+                              kEvictLast);
+          if (++s == C::NS) { s = 0; ++round; }
+        }
+      }
+      ++act;
+    }
+   } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t q_addr = smem_u32(sQ);
+    const uint32_t kv_addr = smem_u32(sKV);
+    const uint64_t dK = sdesc_sw128(kv_addr, 16, 1024);
+    const uint64_t dQ = sdesc_sw128(q_addr, 16, 1024);
+    const uint64_t dV = sdesc_sw128(kv_addr, C::BOX, 1024);
+    auto qk = [&](int h, int stage) {
+      const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
+      const uint64_t b0 = dK + static_cast<uint32_t>((stage * C::TILE) >> 4);
+      #pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
+        mma_ss_elect(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
+      }
+    };
+    constexpr int KPC = 8 / C::NPC;
+    auto pv = [&](int h, int stage, int kh, bool acc) {
+      const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
+      #pragma unroll
+      for (int k4 = 0; k4 < KPC; ++k4) {
+        const int kk = kh * KPC + k4;
+        mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
+                     C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+      }
+    };
+    uint32_t act = 0;
+    uint64_t T = 0;                       // kv tiles of earlier items (per-tile phases)
+    // O_h of the previous item must have been read by its epilogue before the
+    // first (non-accumulating) P.V of this item overwrites it
+    auto pv_both = [&](int h, int stage, uint64_t tile, bool acc) {
+      if (!acc) {
+        mbar_wait(&o_free[h], (act & 1) ^ 1);
+        tc_fence_after();
+      }
+      #pragma unroll
+      for (int kh = 0; kh < C::NPC; ++kh) {
+        mbar_wait(&p_full[C::NPC * h + kh], static_cast<uint32_t>(tile & 1));
+        tc_fence_after();
+        pv(h, stage, kh, acc || kh > 0);
+      }
+    };
+    int sk = 0;
+    uint32_t rk = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      int head, qseg;
+      int64_t qrow0;
+      cta_tile(p, item, head, qseg, qrow0);
+      const tr_segment Q = p.q[qseg];
+      const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
+      const int ntiles = item_kv_tiles<D>(p, qmax_pos, lane, my_tiles);
+      if (ntiles == 0) continue;
+      mbar_wait(q_full, act & 1);
+      tc_fence_after();
+      int prev_v_stage = 0;
+      for (int j = 0; j < ntiles; ++j) {
+        const int sv = (sk + 1 == C::NS) ? 0 : sk + 1;
+        const uint32_t rv = (sk + 1 == C::NS) ? rk + 1 : rk;
+        mbar_wait(&kv_full[sk], rk & 1);
+        tc_fence_after();
+        qk(0, sk);
+        tc_commit_elect(&s_full[0]);
+        if (j > 0) {
+          pv_both(1, prev_v_stage, T + j - 1, j - 1 > 0);
+          tc_commit_elect(&kv_empty[prev_v_stage]);
+        }
+        qk(1, sk);
+        tc_commit_elect(&s_full[1]);
+        tc_commit_elect(&kv_empty[sk]);
+        if (j == ntiles - 1) tc_commit_elect(q_empty);   // sQ free for the next item
+        mbar_wait(&kv_full[sv], rv & 1);
+        pv_both(0, sv, T + j, j > 0);
+        if (j == ntiles - 1) tc_commit_elect(&o_done[0]);
+        prev_v_stage = sv;
+        sk = (sv + 1 == C::NS) ? 0 : sv + 1;
+        rk = (sv + 1 == C::NS) ? rv + 1 : rv;
+      }
+      pv_both(1, prev_v_stage, T + ntiles - 1, ntiles - 1 > 0);
+      tc_commit_elect(&kv_empty[prev_v_stage]);
+      tc_commit_elect(&o_done[1]);
+      T += ntiles;
+      ++act;
+    }
+   }
+  } else {
+   setmaxnreg_inc<224>();
+   {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int h = (warp - 4) / 4;
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + h * 128;
+    const uint32_t tO = tmem + lane_base + 256 + h * 128;
+    const float c = p.scale_log2;
+    const float thresh = C::RESCALE_LOG2 / c;
+    const uint64_t c2 = f2pack(c, c);
+    uint32_t act = 0;
+    uint64_t T = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      int head, qseg;
+      int64_t qrow0;
+      cta_tile(p, item, head, qseg, qrow0);
+      const tr_segment Q = p.q[qseg];
+      const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
+      const int ntiles = item_kv_tiles<D>(p, qmax_pos, lane, my_tiles);
+      const int64_t row_in_seg = qrow0 + 128 * h + r;
+      const int64_t my_pos = Q.pos0 + row_in_seg;
+      const int64_t half_min_pos = Q.pos0 + qrow0 + 128 * h;
+      float m_used = -INFINITY;
+      uint64_t lsum2[2] = {0ull, 0ull};
+      KvWalk w = kv_begin(my_tiles);
+      for (int j = 0; j < ntiles; ++j, w.next(my_tiles)) {
+        const int64_t kpos = p.kv[w.g].pos0 + w.t * 128;
+        const int valid = static_cast<int>(imin64(128, p.kv[w.g].rows - w.t * 128));
+        mbar_wait(&s_full[h], static_cast<uint32_t>((T + j) & 1));
+        tc_fence_after();
+        uint32_t s[128];
+        tmem_ld32_at<0>(tS + 0, s);
+        tmem_ld32_at<32>(tS + 32, s);
+        tmem_ld32_at<64>(tS + 64, s);
+        tmem_ld32_at<96>(tS + 96, s);
+        tc_wait_ld();
+        const bool need_mask = valid < 128 || (p.causal && kpos + 127 > half_min_pos);
+        if (need_mask) {
+          int64_t lim = valid;
+          if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
+          const int limit = static_cast<int>(imax64(lim, 0));
+          #pragma unroll
+          for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;
+        }
+        float mx = __uint_as_float(s[0]);
+        float mxb = __uint_as_float(s[1]);
+        #pragma unroll
+        for (int i = 2; i < 128; i += 4) {
+          mx = fmaxf(mx, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
+          mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
+        }
+        mx = fmaxf(mx, mxb);
+        const bool grow = mx > m_used + thresh;
+        const bool scale_o = grow && m_used != -INFINITY;
+        if (__any_sync(0xffffffffu, scale_o)) {
+          // this tile's S commit implies every earlier MMA (this item's P.V
+          // products included) has completed: O is quiescent
+          const float f = scale_o ? ex2_approx((m_used - mx) * c) : 1.f;
+          const uint64_t f2 = f2pack(f, f);
+          lsum2[0] = fmul2(lsum2[0], f2);
+          lsum2[1] = fmul2(lsum2[1], f2);
+          #pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t u[32];
+            tmem_ld32(tO + cc * 32, u);
+            tc_wait_ld();
+            #pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const uint64_t v = fmul2(f2pack(__uint_as_float(u[i]), __uint_as_float(u[i + 1])), f2);
+              u[i] = static_cast<uint32_t>(v);
+              u[i + 1] = static_cast<uint32_t>(v >> 32);
+            }
+            tmem_st32(tO + cc * 32, u);
+          }
+        }
+        if (grow) m_used = mx;
+        const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
+        const uint64_t nmc2 = f2pack(-mc, -mc);
+        if (need_mask)
+          emit_p<C::POLY_MOD, false, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
+        else
+          emit_p<C::POLY_MOD, true, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
+      }
+      float l;
+      {
+        float a0, a1, b0, b1;
+        f2unpack(lsum2[0], a0, a1);
+        f2unpack(lsum2[1], b0, b1);
+        l = (a0 + a1) + (b0 + b1);
+      }
+      // ---------------------------------------------------------- epilogue
+      const bool row_ok = row_in_seg < Q.rows;
+      const int64_t grow = Q.row0 + row_in_seg;
+      const int64_t oidx = (grow * p.heads + head) * D;
+      const float inv = (l > 0.f) ? 1.f / l : 0.f;
+      uint32_t u[D];
+      if (ntiles > 0) {
+        mbar_wait(&o_done[h], act & 1);
+        tc_fence_after();
+        tmem_ld32_at<0>(tO, u);
+        tmem_ld32_at<32>(tO + 32, u);
+        if constexpr (D == 128) {
+          tmem_ld32_at<64>(tO + 64, u);
+          tmem_ld32_at<96>(tO + 96, u);
+        }
+        tc_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&o_free[h]);          // the next item's P.V may overwrite O_h
+      } else {
+        #pragma unroll
+        for (int i = 0; i < D; ++i) u[i] = 0u;
+      }
+      if (row_ok) {
+        if (p.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oidx);
+          #pragma unroll
+          for (int i = 0; i < D / 4; ++i)
+            dst[i] = make_float4(__uint_as_float(u[4 * i]) * inv, __uint_as_float(u[4 * i + 1]) * inv,
+                                 __uint_as_float(u[4 * i + 2]) * inv, __uint_as_float(u[4 * i + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oidx);
+          #pragma unroll
+          for (int i = 0; i < D / 8; ++i)
+            dst[i] = make_uint4(pack_bf16x2(__uint_as_float(u[8 * i]) * inv, __uint_as_float(u[8 * i + 1]) * inv),
+                                pack_bf16x2(__uint_as_float(u[8 * i + 2]) * inv, __uint_as_float(u[8 * i + 3]) * inv),
+                                pack_bf16x2(__uint_as_float(u[8 * i + 4]) * inv, __uint_as_float(u[8 * i + 5]) * inv),
+                                pack_bf16x2(__uint_as_float(u[8 * i + 6]) * inv, __uint_as_float(u[8 * i + 7]) * inv));
+        }
+        p.lse[head * p.lse_stride + grow] = (l > 0.f) ? (logf(l) + m_used * p.scale) : -INFINITY;
+      }
+      T += ntiles;
+      if (ntiles > 0) ++act;
+    }
+   }
+  }
+  tc_fence_before();
+  if (p.done_flag) __threadfence_system();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -924,6 +1299,18 @@ bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const
   return true;
 }
 
+// one-CTA-per-item grid vs persistent CTAs: build default, overridable at run
+// time with TR_ATTN_PERSISTENT=0/1 (A/B and fallback switch)
+static bool use_persistent() {
+#ifdef TR_PERSISTENT_DEFAULT
+  bool v = TR_PERSISTENT_DEFAULT != 0;
+#else
+  bool v = false;
+#endif
+  if (const char* e = getenv("TR_ATTN_PERSISTENT")) v = e[0] == '1';
+  return v;
+}
+
 template <int D>
 static int launch_d(const void* q, const void* k, const void* v, int64_t tq_total, int64_t tk_total,
                     AttnPlan& plan, cudaStream_t s) {
@@ -939,11 +1326,23 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_sm100)");
+    e = cudaFuncSetAttribute(attn_fwd_persistent_kernel<D>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_persistent)");
     attr_done = true;
   }
   const int64_t blocks = plan.tile_prefix[plan.nq] * plan.heads;
   if (blocks == 0) return TR_OK;
   if (blocks > 0x7FFFFFFF) return fail(TR_ERR_UNSUPPORTED, "grid too large");
+  if (use_persistent()) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+    const int64_t grid = blocks < sms ? blocks : sms;
+    attn_fwd_persistent_kernel<D><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
+    return cuda_status(cudaGetLastError(), "attn_fwd_persistent launch");
+  }
   attn_fwd_sm100_kernel<D><<<static_cast<unsigned>(blocks), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
   return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
 }

@@ -3,8 +3,11 @@
 // (core.py:96-119 DimensionError, partition.py:59-62 ConfigError) so the
 // Python wrapper can map status codes onto the same exception classes.
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cmath>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "tr_internal.h"
 
@@ -43,6 +46,47 @@ static int check_segments(const tr_segment* segs, int n, int64_t total, const ch
       return fail(TR_ERR_DIMENSION, std::string(what) + ": segment outside the buffer");
   }
   return TR_OK;
+}
+
+// Longest-processing-time-first CTA order for a causal launch with several q
+// segments (a TokenRing step: the rows of a light and a heavy chunk in one
+// grid).  Head-major order would run each head's heavy tiles after its light
+// ones, leaving the heaviest CTAs of the last head as the grid's tail; instead
+// every (segment, tile) class is ranked by its kv-tile count and the grid walks
+// the classes heaviest first, heads innermost, in head groups small enough
+// that a group's K/V stays resident in L2.
+static void order_ctas(AttnPlan& plan, int head_dim) {
+  plan.n_order = 0;
+#ifdef TR_NO_ORDER
+  return;   // A/B switch: the plain head-major order
+#endif
+  const int64_t nt = plan.tile_prefix[plan.nq];
+  if (!plan.causal || plan.nq < 2 || nt > TR_ORDER_MAX) return;
+  std::vector<std::pair<int64_t, int>> work;
+  work.reserve(nt);
+  for (int sg = 0; sg < plan.nq; ++sg) {
+    const tr_segment& Q = plan.q[sg];
+    for (int64_t t = 0; t < plan.tile_prefix[sg + 1] - plan.tile_prefix[sg]; ++t) {
+      const int64_t qmax = Q.pos0 + std::min<int64_t>(t * 256 + 255, Q.rows - 1);
+      int64_t n = 0;
+      for (int g = 0; g < plan.nkv; ++g) {
+        const tr_segment& K = plan.kv[g];
+        if (qmax < K.pos0) continue;
+        n += std::min<int64_t>((K.rows + 127) / 128, (qmax - K.pos0) / 128 + 1);
+      }
+      work.emplace_back(-n, static_cast<int>(plan.tile_prefix[sg] + t));
+    }
+  }
+  std::stable_sort(work.begin(), work.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  for (int64_t i = 0; i < nt; ++i) plan.order[i] = static_cast<uint16_t>(work[i].second);
+  int64_t kv_rows = 0;
+  for (int g = 0; g < plan.nkv; ++g) kv_rows += plan.kv[g].rows;
+  const int64_t kv_bytes_per_head = std::max<int64_t>(1, kv_rows * head_dim * 2 * 2);
+  const int64_t budget = 48ll << 20;     // of the 126 MB L2
+  plan.head_group = static_cast<int32_t>(
+      std::max<int64_t>(1, std::min<int64_t>(plan.heads, budget / kv_bytes_per_head)));
+  plan.n_order = static_cast<int32_t>(nt);
 }
 
 // Push options of tr_attention_segments_push (all zero for a local launch).
@@ -97,6 +141,7 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   plan.tile_prefix[0] = 0;
   for (int i = 0; i < plan.nq; ++i)
     plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
+  order_ctas(plan, head_dim);
   if (sm100_supports(head_dim, heads, q, k, v, out) && plan.nkv > 0) {
     // the kernel raises done_flag itself (last CTA); an empty grid does not run
     if ((rc = launch_attn_sm100(q, k, v, tq_total, tk_total, head_dim, plan, s))) return rc;

@@ -8,6 +8,8 @@
 
 namespace tr {
 
+constexpr int TR_ORDER_MAX = 2048;   // (segment, tile) classes an explicit CTA order can hold
+
 // thread-local last error (tr_last_error)
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
@@ -33,6 +35,14 @@ struct AttnPlan {
   unsigned int* done_count;
   unsigned long long* done_flag;
   unsigned long long done_value;
+  // Longest-first CTA order for multi-segment causal launches (n_order > 0):
+  // heads in groups of `head_group` (so a group's K/V stays in L2); inside a
+  // group the (segment, tile) classes run in order[] -- sorted by decreasing
+  // kv-tile count -- with the group's heads innermost.  n_order == 0: the
+  // plain order (head-major, each causal segment heaviest tile first).
+  int32_t n_order;
+  int32_t head_group;
+  uint16_t order[TR_ORDER_MAX];
 };
 
 // last-CTA completion signal of a pushing launch (see AttnPlan::done_flag);

@@ -28,7 +28,7 @@ def bench(fn, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--case", type=int, default=-1, help="run only this case index")
+    ap.add_argument("--case", type=int, nargs="*", default=[], help="run only these case indices")
     a = ap.parse_args()
     cases = [
         ("causal S=32768 H=32 D=128", 32768, 32768, 32, 128, 2),
@@ -36,9 +36,14 @@ def main():
         ("full 16384x8192 H=32 D=128", 16384, 8192, 32, 128, 0),
         ("causal S=131072 H=32 D=128", 131072, 131072, 32, 128, 2),
         ("full 4096x4096 H=8 D=64", 4096, 4096, 8, 64, 0),
+        # per-CTA fixed cost: same flops, 256 / 128 / 64 / 32 kv tiles per CTA
+        ("full 4096x32768 H=32 D=128", 4096, 32768, 32, 128, 0),
+        ("full 8192x16384 H=32 D=128", 8192, 16384, 32, 128, 0),
+        ("full 16384x8192 H=32 D=128", 16384, 8192, 32, 128, 0),
+        ("full 32768x4096 H=32 D=128", 32768, 4096, 32, 128, 0),
     ]
-    if a.case >= 0:
-        cases = [cases[a.case]]
+    if a.case:
+        cases = [cases[i] for i in a.case]
     for name, tq, tk, h, d, mask in cases:
         q = torch.randn(tq, h, d, device="cuda").to(torch.bfloat16) * 0.5
         k = torch.randn(tk, h, d, device="cuda").to(torch.bfloat16) * 0.5
