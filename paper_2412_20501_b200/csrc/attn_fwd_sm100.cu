@@ -289,8 +289,16 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       #pragma unroll
       for (int k4 = 0; k4 < KPC; ++k4) {
         const int kk = kh * KPC + k4;
+#if defined(TR_EXP_NOSOFTMAX) && defined(TR_EXP_PSMEM)
+        // experiment: A (P) from shared memory, SS mode
+        const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
+        const uint32_t offa = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
+        mma_ss_elect(tmem + 256 + h * 128, desc_add(a0, offa), desc_add(b0, (kk * 2048) >> 4),
+                     C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+#else
         mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
                      C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+#endif
       }
     };
     auto pv_both = [&](int h, int stage, uint32_t phase, bool acc) {
@@ -359,6 +367,20 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       tc_fence_after();
 #ifdef TR_EXP_NOSOFTMAX
       // experiment: measure the MMA/TMA pipeline alone (results are garbage)
+#ifdef TR_EXP_PSMEM
+      // ... with P written to shared memory (this half's Q tile stands in for
+      // the P buffer: 256 B per row, 128B-swizzled K-major) for an SS-mode P.V
+      {
+        uint8_t* prow = sQ + h * C::TILE;
+        #pragma unroll
+        for (int c16 = 0; c16 < 16; ++c16) {
+          const int box = c16 / 8, chunk = c16 % 8;
+          uint4* dst = reinterpret_cast<uint4*>(prow + box * C::BOX + r * 128 + ((chunk ^ (r & 7)) * 16));
+          *dst = make_uint4(r, c16, j, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+#endif
       tc_fence_before();
       for (int kh = 0; kh < C::NPC; ++kh) mbar_arrive(&p_full[C::NPC * h + kh]);
       continue;
@@ -491,6 +513,395 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   }
   tc_fence_before();
   if (p.done_flag) __threadfence_system();   // out/lse rows may live on a peer GPU
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+  if (p.done_flag && threadIdx.x == 0) signal_done(p);
+}
+
+// ============================================================================
+// attn_fwd_ps_kernel (D = 128): P goes to SHARED memory instead of TMEM.
+//
+// In attn_fwd_sm100_kernel P_h overwrites S_h's TMEM columns, so the next
+// QK_h cannot be issued before P_h.V has read P_h: per half, every kv tile
+// pays QK (512 tensor cycles) + softmax (~1650) + P.V (512) + barrier
+// latencies back to back, a ~3300-cycle period against 2048 cycles of tensor
+// work.  With P in shared memory (its own 2 x 32 KB, 128B-swizzled K-major
+// like a Q tile; the P.V MMA reads A from smem, SS mode), S_h is free as soon
+// as the softmax warps have loaded it into registers (s_free), so QK_h(j+1)
+// runs while softmax_h(j) exponentiates, and the per-tile period becomes
+// max(tensor 2048, softmax) -- the softmax of both halves now run side by
+// side.  Measured with the softmax stubbed out (TR_EXP_NOSOFTMAX
+// TR_EXP_PSMEM): SS-mode P.V + the P stores cost ~4 % of the pipeline's
+// throughput, i.e. shared memory keeps up.
+// Smem: Q 64 KB + P 64 KB + a 3-stage K/V ring (96 KB) consumed in the order
+// K0 K1 V0 K2 V1 K3 V2 ...: every slot is released long before it is
+// reloaded (V_j reuses K_j's slot, K_{j+2} reuses V_{j-1}'s).
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
+// MMA order per tile j: QK0(j+1) QK1(j+1) | P0a.V P1a.V P0b.V P1b.V (j)
+// (a/b = 64-key chunks; each chunk has its own full/free barrier so the
+// softmax can refill chunk a of P while P.V still reads chunk b).
+struct PsCfg {
+  static constexpr int D = 128;
+  static constexpr int BOX = 128 * 64 * 2;        // 16 KB: 128 rows x 64 bf16
+  static constexpr int TILE = 2 * BOX;            // 32 KB: 128 rows x 128 bf16
+  static constexpr int NS = 3;                    // K/V ring stages
+  static constexpr int THREADS = 384;
+  static constexpr int SMEM_TILES = (2 + 2 + NS) * TILE;   // Q0 Q1 P0 P1 ring
+  static constexpr int SMEM = SMEM_TILES + 1024 + 1024;
+  static constexpr uint32_t IDESC_QK = idesc_bf16(128, 128, false);
+  static constexpr uint32_t IDESC_PV = idesc_bf16(128, 128, true);
+  static constexpr float RESCALE_LOG2 = 8.0f;
+  static constexpr int POLY_MOD = TR_POLY_MOD;
+};
+
+// exp2 of 64 scores (one P chunk of a row) -> 8 swizzled 16-byte stores into
+// the P tile; row sums accumulate in lsum2.
+template <int POLY_MOD, bool kPoly>
+__device__ __forceinline__ void p_chunk_smem(const uint32_t (&s)[128], int kh, uint64_t c2,
+                                             uint64_t nmc2, uint64_t (&lsum2)[2], uint8_t* prow,
+                                             int r) {
+  #pragma unroll
+  for (int c16 = 0; c16 < 8; ++c16) {
+    uint32_t w[4];
+    #pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int i = kh * 32 + c16 * 4 + q4;     // pair index in the row
+      const uint64_t x2 = ffma2(f2pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nmc2);
+      float a, b;
+      f2unpack(x2, a, b);
+      uint64_t p2;
+      if (kPoly && (i % POLY_MOD) == POLY_MOD - 1)
+        p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f)));
+      else
+        p2 = f2pack(ex2_approx(a), ex2_approx(b));
+      lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
+      float pa, pb;
+      f2unpack(p2, pa, pb);
+      w[q4] = pack_bf16x2(pa, pb);
+    }
+    *reinterpret_cast<uint4*>(prow + kh * PsCfg::BOX + r * 128 + ((c16 ^ (r & 7)) * 16)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__global__ void __launch_bounds__(384, 1)
+attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+                   const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnPlan p) {
+  using C = PsCfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                        // 2 tiles
+  uint8_t* sP = smem + 2 * C::TILE;          // 2 tiles
+  uint8_t* sKV = smem + 4 * C::TILE;         // NS tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_TILES);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;              // [NS]
+  uint64_t* kv_empty = kv_full + C::NS;      // [NS]
+  uint64_t* s_full = kv_empty + C::NS;       // [2]
+  uint64_t* s_free = s_full + 2;             // [2]
+  uint64_t* p_full = s_free + 2;             // [2 halves][2 chunks]
+  uint64_t* p_free = p_full + 4;             // [2 halves][2 chunks]
+  uint64_t* o_done = p_free + 4;             // [2]
+  int64_t* kv_tiles = reinterpret_cast<int64_t*>(o_done + 2);   // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_tiles + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  int head, qseg;
+  int64_t qrow0;
+  cta_tile(p, blockIdx.x, head, qseg, qrow0);
+  const tr_segment Q = p.q[qseg];
+  const int64_t qmax_pos = Q.pos0 + imin64(qrow0 + 255, Q.rows - 1);
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&s_full[h], 1);
+      mbar_init(&s_free[h], 128);
+      mbar_init(&o_done[h], 1);
+      for (int c = 0; c < 2; ++c) {
+        mbar_init(&p_full[2 * h + c], 128);
+        mbar_init(&p_free[2 * h + c], 1);
+      }
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmq); tma_prefetch_desc(&tmk); tma_prefetch_desc(&tmv);
+  }
+  if (warp == 2 && lane < TR_MAX_SEGMENTS) {
+    int64_t n = 0;
+    if (lane < p.nkv) {
+      n = (p.kv[lane].rows + 127) / 128;
+      if (p.causal)
+        n = (qmax_pos < p.kv[lane].pos0) ? 0 : imin64(n, (qmax_pos - p.kv[lane].pos0) / 128 + 1);
+    }
+    kv_tiles[lane] = n;
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const int ntiles = __shfl_sync(
+      0xffffffffu, static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]), 0);
+
+  if (warp < 4) {
+   setmaxnreg_dec<56>();
+   if (warp == 0 && ntiles > 0) {
+    // ------------------------------------------------------------ producer
+    const int32_t col0 = head * D;
+    mbar_arrive_expect_tx_elect(q_full, 2 * C::TILE);
+    for (int h = 0; h < 2; ++h)
+      for (int b = 0; b < 2; ++b)
+        tma_load_2d_elect(sQ + (h * 2 + b) * C::BOX, &tmq, q_full, col0 + 64 * b,
+                          static_cast<int32_t>(Q.row0 + qrow0 + 128 * h), kEvictFirst);
+    int s = 0;
+    uint32_t round = 0;
+    auto put = [&](const CUtensorMap* tm, int64_t krow) {
+      mbar_wait(&kv_empty[s], (round & 1) ^ 1);
+      mbar_arrive_expect_tx_elect(&kv_full[s], C::TILE);
+      for (int b = 0; b < 2; ++b)
+        tma_load_2d_elect(sKV + s * C::TILE + b * C::BOX, tm, &kv_full[s], col0 + 64 * b,
+                          static_cast<int32_t>(krow), kEvictLast);
+      if (++s == C::NS) { s = 0; ++round; }
+    };
+    // consumption order: K0 K1 V0 K2 V1 K3 V2 ...
+    KvWalk wk = kv_begin(kv_tiles), wv = wk;
+    put(&tmk, p.kv[wk.g].row0 + wk.t * 128);                 // K0
+    wk.next(kv_tiles);
+    if (ntiles > 1) {
+      put(&tmk, p.kv[wk.g].row0 + wk.t * 128);               // K1
+      wk.next(kv_tiles);
+    }
+    for (int j = 0; j < ntiles; ++j) {
+      put(&tmv, p.kv[wv.g].row0 + wv.t * 128);               // V_j
+      wv.next(kv_tiles);
+      if (j + 2 < ntiles) {
+        put(&tmk, p.kv[wk.g].row0 + wk.t * 128);             // K_{j+2}
+        wk.next(kv_tiles);
+      }
+    }
+   } else if (warp == 1 && ntiles > 0) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint64_t dQ = sdesc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t dP = sdesc_sw128(smem_u32(sP), 16, 1024);
+    const uint64_t dK = sdesc_sw128(smem_u32(sKV), 16, 1024);
+    const uint64_t dV = sdesc_sw128(smem_u32(sKV), C::BOX, 1024);
+    int n_idx = 0;
+    auto take = [&]() {
+      const int slot = n_idx % C::NS;
+      mbar_wait(&kv_full[slot], static_cast<uint32_t>((n_idx / C::NS) & 1));
+      tc_fence_after();
+      ++n_idx;
+      return slot;
+    };
+    auto qk = [&](int h, int slot) {
+      const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
+      const uint64_t b0 = dK + static_cast<uint32_t>((slot * C::TILE) >> 4);
+      #pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
+        mma_ss_elect(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
+      }
+    };
+    // O_h += P_h[:, chunk c keys] . V[chunk c keys, :]   (A from smem)
+    auto pv = [&](int h, int slot, int c, bool acc) {
+      const uint64_t a0 = dP + static_cast<uint32_t>((h * C::TILE) >> 4);
+      const uint64_t b0 = dV + static_cast<uint32_t>((slot * C::TILE) >> 4);
+      #pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const int kk = c * 4 + k4;
+        const uint32_t offa = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
+        mma_ss_elect(tmem + 256 + h * 128, desc_add(a0, offa), desc_add(b0, (kk * 2048) >> 4),
+                     C::IDESC_PV, (acc || k4 > 0) ? 1u : 0u);
+      }
+    };
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    int ks = take();                                          // K0
+    qk(0, ks);
+    tc_commit_elect(&s_full[0]);
+    qk(1, ks);
+    tc_commit_elect(&s_full[1]);
+    tc_commit_elect(&kv_empty[ks]);
+    for (int j = 0; j < ntiles; ++j) {
+      const uint32_t ph = j & 1;
+      if (j + 1 < ntiles) {
+        ks = take();                                          // K_{j+1}
+        mbar_wait(&s_free[0], ph);
+        tc_fence_after();
+        qk(0, ks);
+        tc_commit_elect(&s_full[0]);
+        mbar_wait(&s_free[1], ph);
+        tc_fence_after();
+        qk(1, ks);
+        tc_commit_elect(&s_full[1]);
+        tc_commit_elect(&kv_empty[ks]);
+      }
+      const int vs = take();                                  // V_j
+      #pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        #pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&p_full[2 * h + c], ph);
+          tc_fence_after();
+          pv(h, vs, c, j > 0 || c > 0);
+          tc_commit_elect(&p_free[2 * h + c]);
+        }
+      }
+      tc_commit_elect(&kv_empty[vs]);
+    }
+    tc_commit_elect(&o_done[0]);
+    tc_commit_elect(&o_done[1]);
+   }
+  } else {
+   setmaxnreg_inc<224>();
+   {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int h = (warp - 4) / 4;
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + h * 128;
+    const uint32_t tO = tmem + lane_base + 256 + h * 128;
+    uint8_t* prow = sP + h * C::TILE;
+    const int64_t row_in_seg = qrow0 + 128 * h + r;
+    const int64_t my_pos = Q.pos0 + row_in_seg;
+    const int64_t half_min_pos = Q.pos0 + qrow0 + 128 * h;
+    const float c = p.scale_log2;
+    const float thresh = C::RESCALE_LOG2 / c;
+    const uint64_t c2 = f2pack(c, c);
+    float m_used = -INFINITY;
+    uint64_t lsum2[2] = {0ull, 0ull};
+    KvWalk w = kv_begin(kv_tiles);
+    for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
+      const uint32_t ph = j & 1;
+      const int64_t kpos = p.kv[w.g].pos0 + w.t * 128;
+      const int valid = static_cast<int>(imin64(128, p.kv[w.g].rows - w.t * 128));
+      mbar_wait(&s_full[h], ph);
+      tc_fence_after();
+      uint32_t s[128];
+      tmem_ld32_at<0>(tS + 0, s);
+      tmem_ld32_at<32>(tS + 32, s);
+      tmem_ld32_at<64>(tS + 64, s);
+      tmem_ld32_at<96>(tS + 96, s);
+      tc_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_free[h]);            // S_h may now be overwritten by QK_h(j+1)
+      const bool need_mask = valid < 128 || (p.causal && kpos + 127 > half_min_pos);
+      if (need_mask) {
+        int64_t lim = valid;
+        if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
+        const int limit = static_cast<int>(imax64(lim, 0));
+        #pragma unroll
+        for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;
+      }
+      float mx = __uint_as_float(s[0]);
+      float mxb = __uint_as_float(s[1]);
+      #pragma unroll
+      for (int i = 2; i < 128; i += 4) {
+        mx = fmaxf(mx, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
+        mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
+      }
+      mx = fmaxf(mx, mxb);
+      const bool grow = mx > m_used + thresh;
+      const bool scale_o = grow && m_used != -INFINITY;
+      if (__any_sync(0xffffffffu, scale_o)) {
+        // O_h must hold every P.V of earlier tiles: wait for the last chunk
+        // of P_h(j-1).V (the chunks complete in order)
+        mbar_wait(&p_free[2 * h + 1], ph ^ 1);
+        tc_fence_after();
+        const float f = scale_o ? ex2_approx((m_used - mx) * c) : 1.f;
+        const uint64_t f2 = f2pack(f, f);
+        lsum2[0] = fmul2(lsum2[0], f2);
+        lsum2[1] = fmul2(lsum2[1], f2);
+        #pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t u[32];
+          tmem_ld32(tO + cc * 32, u);
+          tc_wait_ld();
+          #pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t v = fmul2(f2pack(__uint_as_float(u[i]), __uint_as_float(u[i + 1])), f2);
+            u[i] = static_cast<uint32_t>(v);
+            u[i + 1] = static_cast<uint32_t>(v >> 32);
+          }
+          tmem_st32(tO + cc * 32, u);
+        }
+        tc_wait_st();
+      }
+      if (grow) m_used = mx;
+      const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
+      const uint64_t nmc2 = f2pack(-mc, -mc);
+      #pragma unroll
+      for (int kh = 0; kh < 2; ++kh) {
+        // P_h(j-1).V has finished reading this chunk of the P tile
+        mbar_wait(&p_free[2 * h + kh], ph ^ 1);
+        if (need_mask)
+          p_chunk_smem<C::POLY_MOD, false>(s, kh, c2, nmc2, lsum2, prow, r);
+        else
+          p_chunk_smem<C::POLY_MOD, true>(s, kh, c2, nmc2, lsum2, prow, r);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * h + kh]);
+      }
+    }
+    float l;
+    {
+      float a0, a1, b0, b1;
+      f2unpack(lsum2[0], a0, a1);
+      f2unpack(lsum2[1], b0, b1);
+      l = (a0 + a1) + (b0 + b1);
+    }
+    // ---------------------------------------------------------- epilogue
+    const bool row_ok = row_in_seg < Q.rows;
+    const int64_t grow = Q.row0 + row_in_seg;
+    const int64_t oidx = (grow * p.heads + head) * D;
+    if (ntiles > 0) {
+      mbar_wait(&o_done[h], 0);
+      tc_fence_after();
+    }
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    #pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t u[32];
+      if (ntiles > 0) {
+        tmem_ld32(tO + cc * 32, u);
+        tc_wait_ld();
+      } else {
+        #pragma unroll
+        for (int i = 0; i < 32; ++i) u[i] = 0u;
+      }
+      if (p.out_f32) {
+        if (row_ok) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oidx + cc * 32);
+          #pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(u[4 * i]) * inv, __uint_as_float(u[4 * i + 1]) * inv,
+                                 __uint_as_float(u[4 * i + 2]) * inv, __uint_as_float(u[4 * i + 3]) * inv);
+        }
+        continue;
+      }
+      uint32_t pk[16];
+      #pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(__uint_as_float(u[2 * i]) * inv, __uint_as_float(u[2 * i + 1]) * inv);
+      if (row_ok) {
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oidx + cc * 32);
+        #pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+    if (row_ok)
+      p.lse[head * p.lse_stride + grow] = (l > 0.f) ? (logf(l) + m_used * p.scale) : -INFINITY;
+   }
+  }
+  tc_fence_before();
+  if (p.done_flag) __threadfence_system();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -1311,6 +1722,18 @@ static bool use_persistent() {
   return v;
 }
 
+// P in shared memory (attn_fwd_ps_kernel) vs in TMEM: build default,
+// overridable at run time with TR_ATTN_PSMEM=0/1
+static bool use_psmem() {
+#ifdef TR_PSMEM_DEFAULT
+  bool v = TR_PSMEM_DEFAULT != 0;
+#else
+  bool v = false;
+#endif
+  if (const char* e = getenv("TR_ATTN_PSMEM")) v = e[0] == '1';
+  return v;
+}
+
 template <int D>
 static int launch_d(const void* q, const void* k, const void* v, int64_t tq_total, int64_t tk_total,
                     AttnPlan& plan, cudaStream_t s) {
@@ -1334,6 +1757,17 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
   const int64_t blocks = plan.tile_prefix[plan.nq] * plan.heads;
   if (blocks == 0) return TR_OK;
   if (blocks > 0x7FFFFFFF) return fail(TR_ERR_UNSUPPORTED, "grid too large");
+  if (D == 128 && use_psmem()) {
+    static bool ps_attr = false;
+    if (!ps_attr) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd_ps_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, PsCfg::SMEM);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_ps)");
+      ps_attr = true;
+    }
+    attn_fwd_ps_kernel<<<static_cast<unsigned>(blocks), PsCfg::THREADS, PsCfg::SMEM, s>>>(tq, tk, tv, plan);
+    return cuda_status(cudaGetLastError(), "attn_fwd_ps launch");
+  }
   if (use_persistent()) {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
