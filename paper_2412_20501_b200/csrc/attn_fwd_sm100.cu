@@ -543,6 +543,11 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
 // MMA order per tile j: QK0(j+1) QK1(j+1) | P0a.V P1a.V P0b.V P1b.V (j)
 // (a/b = 64-key chunks; each chunk has its own full/free barrier so the
 // softmax can refill chunk a of P while P.V still reads chunk b).
+#ifndef TR_PS_SPLIT
+#define TR_PS_SPLIT 0
+#endif
+constexpr int kPsIssuers = TR_PS_SPLIT ? 2 : 1;   // MMA issuer warps (1, or one per half)
+
 struct PsCfg {
   static constexpr int D = 128;
   static constexpr int BOX = 128 * 64 * 2;        // 16 KB: 128 rows x 64 bf16
@@ -619,7 +624,7 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < C::NS; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], kPsIssuers); }
     for (int h = 0; h < 2; ++h) {
       mbar_init(&s_full[h], 1);
       mbar_init(&s_free[h], 128);
@@ -685,8 +690,8 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
         wk.next(kv_tiles);
       }
     }
-   } else if (warp == 1 && ntiles > 0) {
-    // ------------------------------------------------------------ MMA issuer
+   } else if ((warp == 1 || (kPsIssuers == 2 && warp == 3)) && ntiles > 0) {
+    // ------------------------------------------------------------ MMA issuer(s)
     const uint64_t dQ = sdesc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t dP = sdesc_sw128(smem_u32(sP), 16, 1024);
     const uint64_t dK = sdesc_sw128(smem_u32(sKV), 16, 1024);
@@ -722,41 +727,79 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
     };
     mbar_wait(q_full, 0);
     tc_fence_after();
-    int ks = take();                                          // K0
-    qk(0, ks);
-    tc_commit_elect(&s_full[0]);
-    qk(1, ks);
-    tc_commit_elect(&s_full[1]);
-    tc_commit_elect(&kv_empty[ks]);
-    for (int j = 0; j < ntiles; ++j) {
-      const uint32_t ph = j & 1;
-      if (j + 1 < ntiles) {
-        ks = take();                                          // K_{j+1}
-        mbar_wait(&s_free[0], ph);
-        tc_fence_after();
-        qk(0, ks);
-        tc_commit_elect(&s_full[0]);
-        mbar_wait(&s_free[1], ph);
-        tc_fence_after();
-        qk(1, ks);
-        tc_commit_elect(&s_full[1]);
-        tc_commit_elect(&kv_empty[ks]);
-      }
-      const int vs = take();                                  // V_j
-      #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+    if constexpr (kPsIssuers == 2) {
+      // one issuer per half (warp 1: half 0, warp 3: half 1), each in its own
+      // half's natural order; half 1 starts once half 0 has published its
+      // first P chunk, so the two softmax groups run staggered (one
+      // exponentiates while the other loads S / reduces its max)
+      const int h = (warp == 1) ? 0 : 1;
+      int ks = take();                                        // K0
+      if (h == 1) mbar_wait(&p_full[0], 0);
+      qk(h, ks);
+      tc_commit_elect(&s_full[h]);
+      tc_commit_elect(&kv_empty[ks]);
+      for (int j = 0; j < ntiles; ++j) {
+        const uint32_t ph = j & 1;
+        if (j + 1 < ntiles) {
+          ks = take();                                        // K_{j+1}
+          mbar_wait(&s_free[h], ph);
+          tc_fence_after();
+          qk(h, ks);
+          tc_commit_elect(&s_full[h]);
+          tc_commit_elect(&kv_empty[ks]);
+        }
+        const int vs = take();                                // V_j
         #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int c = 0; c < 2; ++c) {
           mbar_wait(&p_full[2 * h + c], ph);
           tc_fence_after();
           pv(h, vs, c, j > 0 || c > 0);
           tc_commit_elect(&p_free[2 * h + c]);
         }
+        tc_commit_elect(&kv_empty[vs]);
       }
-      tc_commit_elect(&kv_empty[vs]);
+      tc_commit_elect(&o_done[h]);
+    } else {
+      int ks = take();                                          // K0
+      qk(0, ks);
+      tc_commit_elect(&s_full[0]);
+      qk(1, ks);
+      tc_commit_elect(&s_full[1]);
+      tc_commit_elect(&kv_empty[ks]);
+      for (int j = 0; j < ntiles; ++j) {
+        const uint32_t ph = j & 1;
+        TR_TRACE_AT(0, j);
+        if (j + 1 < ntiles) {
+          ks = take();                                          // K_{j+1}
+          mbar_wait(&s_free[0], ph);
+          tc_fence_after();
+          qk(0, ks);
+          tc_commit_elect(&s_full[0]);
+          mbar_wait(&s_free[1], ph);
+          tc_fence_after();
+          qk(1, ks);
+          tc_commit_elect(&s_full[1]);
+          tc_commit_elect(&kv_empty[ks]);
+        }
+        TR_TRACE_AT(1, j);
+        const int vs = take();                                  // V_j
+        TR_TRACE_AT(2, j);
+        #pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(&p_full[2 * h + c], ph);
+            tc_fence_after();
+            pv(h, vs, c, j > 0 || c > 0);
+            tc_commit_elect(&p_free[2 * h + c]);
+          }
+        }
+        tc_commit_elect(&kv_empty[vs]);
+        TR_TRACE_AT(3, j);
+      }
+      tc_commit_elect(&o_done[0]);
+      tc_commit_elect(&o_done[1]);
     }
-    tc_commit_elect(&o_done[0]);
-    tc_commit_elect(&o_done[1]);
    }
   } else {
    setmaxnreg_inc<224>();
@@ -782,8 +825,10 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
       const uint32_t ph = j & 1;
       const int64_t kpos = p.kv[w.g].pos0 + w.t * 128;
       const int valid = static_cast<int>(imin64(128, p.kv[w.g].rows - w.t * 128));
+      TR_TRACE_AT(0, j);
       mbar_wait(&s_full[h], ph);
       tc_fence_after();
+      TR_TRACE_AT(1, j);
       uint32_t s[128];
       tmem_ld32_at<0>(tS + 0, s);
       tmem_ld32_at<32>(tS + 32, s);
@@ -808,6 +853,7 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
         mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
       }
       mx = fmaxf(mx, mxb);
+      TR_TRACE_AT(2, j);
       const bool grow = mx > m_used + thresh;
       const bool scale_o = grow && m_used != -INFINITY;
       if (__any_sync(0xffffffffu, scale_o)) {
@@ -841,6 +887,7 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
       for (int kh = 0; kh < 2; ++kh) {
         // P_h(j-1).V has finished reading this chunk of the P tile
         mbar_wait(&p_free[2 * h + kh], ph ^ 1);
+        TR_TRACE_AT(3 + 2 * kh, j);
         if (need_mask)
           p_chunk_smem<C::POLY_MOD, false>(s, kh, c2, nmc2, lsum2, prow, r);
         else
@@ -848,6 +895,7 @@ attn_fwd_ps_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constan
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&p_full[2 * h + kh]);
+        TR_TRACE_AT(4 + 2 * kh, j);
       }
     }
     float l;
