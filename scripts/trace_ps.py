@@ -23,8 +23,8 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = np.zeros(2 * 12 * 64 * 8, dtype=np.uint64)
 L = _lib.lib()
-L.tr_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-assert L.tr_debug_trace(buf.ctypes.data, buf.nbytes) == 0
+L.tr_debug_trace_variants.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+assert L.tr_debug_trace_variants(buf.ctypes.data, buf.nbytes) == 0
 t = buf.reshape(2, 12, 64, 8)[0].astype(np.int64)
 print("MMA warp (median cycles over tiles 8..60): iter period, start->QK issued, ->V landed, ->PV issued")
 m = t[1][8:60]
