@@ -4,6 +4,7 @@
 #      serialised -- compare shares, not absolutes)
 #   2. one `ncu --set full` capture of the attention kernel at the bench size
 #   3. one `ncu --set full` capture of the lse-merge kernel
+#   4. one `ncu --set full` capture of the n-way merge (fused transport's fold)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -17,4 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_vec8 -c 1 \
   -o gpurun_out/merge_${TAG} -f \
   python scripts/probe_merge.py > gpurun_out/merge_ncu_${TAG}.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_n_vec8 -c 1 \
+  -o gpurun_out/merge_n_${TAG} -f \
+  python scripts/probe_merge.py > gpurun_out/merge_n_ncu_${TAG}.log 2>&1
 ls -la gpurun_out
