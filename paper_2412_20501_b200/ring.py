@@ -279,7 +279,12 @@ class TokenRingAttention:
     # send is a cudaMemcpyAsync straight into the peer's buffer on this rank's
     # copy stream -- copy engines, no SMs taken from the attention kernel --
     # followed by a release store to the peer's sequence flag.
-    #   flags[0]   (unused)
+    # Values are call-relative: call n uses base_n = BASE0 + n*P and every flag
+    # only grows, so consecutive calls need no reset, no device sync and no
+    # barrier -- each flag's value at the end of call n is exactly its initial
+    # condition for call n+1 (set once for call 0 in _ipc_setup).
+    #   flags[0] fin     : base of the last call whose received messages I have
+    #                      folded (fused: a sender may reuse my slots)
     #   flags[1] q_free  : highest step whose traveling-Q slot I am done with
     #   flags[2] o_ready : highest step whose returned OUT for me has landed
     #   flags[3] o_free  : highest step whose returned OUT I have merged
@@ -312,6 +317,18 @@ class TokenRingAttention:
                     kernels.enable_peer_access(peer_dev)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.calls = 0
+        # initial conditions of call 0, visible to every peer before anyone sends
+        b = self._base(0)
+        init = torch.full_like(self.flags, b - 1)
+        init[0] = b - self.P            # "the call before 0" has been folded
+        init[1] = b                     # step 0 runs on q_loc: slot 0 is free
+        init[3] = b + 1                 # ipc: my single OUT receive buffer is free
+        self.flags.copy_(init)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+
+    def _base(self, call):
+        return 2 * self.P + 8 + call * self.P
 
     def _flags_of(self, r):
         return self.flags if r == self.rank else self.peer[r][4]
@@ -338,15 +355,10 @@ class TokenRingAttention:
         c, rank, P, H = self.c, self.rank, self.P, self.H
         fused, fp = self.transport == "fused", self.fplan
         O0 = 4 + P                     # fused: o_ready flag of each receive slot
-        base = self.calls * (P + 4) + 8
+        base = self._base(self.calls)
         self.calls += 1
         cur = torch.cuda.current_stream(self.device)
         cs = self.copy_stream
-        # initial conditions of this call, visible to every peer before anyone sends
-        self.flags[:4] = torch.tensor([base - 1, base, base - 1, base + 1], dtype=torch.int64)
-        self.flags[4:] = base - 1
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)
         if not self.direct_first:
             self.ops.init_(self.acc_out, self.acc_lse)
         local_layout = self.prog[0].q_layout
@@ -422,6 +434,8 @@ class TokenRingAttention:
                     # (the slot holds only message k, and the previous call's
                     # merge of it finished before this call's barrier)
                     k, dst, a, b = fp.push[i]
+                    # the home has folded the previous call's messages out of its slots
+                    kernels.flag_wait_(self._flags_of(dst)[0:1], base - P, cur)
                     slot = self.fplans[dst].slot_of(k)
                     ob, lb = self._recv_slot(slot, dst)
                     ev["o_push_bytes"] = (b - a) * H * (2 * self.D + 4)   # carried by this launch
@@ -462,6 +476,13 @@ class TokenRingAttention:
             n = len(ids) * c
             self._merge_returned((ids, self.out_recv[:n],
                                   self.lse_recv.view(-1)[: H * n].view(H, n)), local_layout)
+        # hand the next call its initial conditions (next base = base + P):
+        # everything received is folded, the OUT buffer is free, and both
+        # traveling-Q slots are free once this call's computes are done
+        kernels.flag_set_(self.flags[0:1], base, cur)
+        kernels.flag_set_(self.flags[3:4], base + P + 1, cur)
+        cs.wait_stream(cur)
+        kernels.flag_set_(self.flags[1:2], base + P, cs)
         cur.wait_stream(cs)
         return Partial(self.acc_out, self.acc_lse)
 

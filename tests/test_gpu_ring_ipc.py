@@ -31,7 +31,14 @@ def _port():
     return p
 
 
+SEEDS = (21, 22, 21)
+
+
 def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
+    """Back-to-back calls with different inputs and no host synchronisation
+    in between (the runner's flags carry each call's initial conditions);
+    rank 0 is delayed on the device before every call so its peers run ahead
+    into the next call -- every call's result must still be its own."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -41,11 +48,15 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
                                     transport=transport, route=route)
-        q, k, v = rng.local_inputs(21, runner.part, rank, H, D)
-        for _ in range(calls):            # repeated calls exercise the flag bases
-            res = runner(q, k, v)
+        inputs = {sd: rng.local_inputs(sd, runner.part, rank, H, D) for sd in set(SEEDS)}
+        outs = []
+        for sd in SEEDS[:calls]:
+            if rank == 0:
+                torch.cuda._sleep(2_000_000)     # ~1 ms of device time
+            res = runner(*inputs[sd])
+            outs.append((res.out.clone(), res.lse.clone()))
         torch.cuda.synchronize()
-        q_out.put((rank, res.out.double().cpu().numpy(), res.lse.double().cpu().numpy()))
+        q_out.put((rank, [(o.double().cpu().numpy(), l.double().cpu().numpy()) for o, l in outs]))
         dist.barrier()
     finally:
         dist.destroy_process_group()
@@ -68,19 +79,24 @@ def test_token_ring_ipc(world, S, H, D, causal, route, transport):
         p.start()
     res = {}
     for _ in range(world):
-        r, o, l = q_out.get(timeout=300)
-        res[r] = (o, l)
+        r, calls_out = q_out.get(timeout=300)
+        res[r] = calls_out
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(21, S, H, D))
     sched = osch.zigzag_token_ring(world, S, H, D) if causal else osch.token_ring(world, S, H, D)
-    ref = osch.execute(sched, q, k, v)
+    refs = {}
+    for sd in set(SEEDS):
+        q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(sd, S, H, D))
+        refs[sd] = osch.execute(sched, q, k, v)
     for r in range(world):
-        assert np.abs(res[r][0] - ref[r][0]).max() <= 2e-2
-        fin = np.isfinite(ref[r][1])
-        assert np.array_equal(np.isfinite(res[r][1]), fin)
-        assert np.abs(res[r][1][fin] - ref[r][1][fin]).max() <= 1e-3
+        for call, sd in enumerate(SEEDS):
+            out, lse = res[r][call]
+            ref = refs[sd][r]
+            assert np.abs(out - ref[0]).max() <= 2e-2, (r, call)
+            fin = np.isfinite(ref[1])
+            assert np.array_equal(np.isfinite(lse), fin)
+            assert np.abs(lse[fin] - ref[1][fin]).max() <= 1e-3, (r, call)
 
 
 def _worker_full(rank, world, port, S, H, D, q_out):
