@@ -8,6 +8,7 @@
 // and every row's D contiguous values go through 16-byte vector accesses.
 #include <cuda_bf16.h>
 #include <cmath>
+#include <type_traits>
 
 #include "tr_internal.h"
 
@@ -219,6 +220,83 @@ __global__ void __launch_bounds__(256) merge_n_vec8_kernel(float* __restrict__ a
         make_uint4(bf16x2(o[0], o[1]), bf16x2(o[2], o[3]), bf16x2(o[4], o[5]), bf16x2(o[6], o[7]));
 }
 
+// Compile-time block count (bf16 partials, N <= 8), 16 values per thread:
+// each partial contributes two 16-byte loads per thread that ptxas issues
+// together, so twice the bytes are in flight per thread than in the generic
+// 8-value loop above (whose -inf test in front of every load also keeps a
+// single load outstanding).  A partial whose lse is -inf contributes weight
+// 0 and its values are never read.
+template <int N>
+__global__ void __launch_bounds__(256) merge_n_bf16_kernel(float* __restrict__ acc_out,
+                                                           const float* __restrict__ acc_lse,
+                                                           const __grid_constant__ MergeN m,
+                                                           int64_t T, int H, int D, int64_t acc_ls,
+                                                           __nv_bfloat16* __restrict__ final_out) {
+  const int per_row = D / 16;
+  const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gid / per_row;
+  if (row >= T * H) return;
+  const int part = static_cast<int>(gid % per_row);
+  const int h = static_cast<int>(row / T);
+  const int64_t t = row % T;
+  const int64_t off = (t * H + h) * D + part * 16;
+  float* ap = acc_out + off;
+  const float a = acc_lse[h * acc_ls + t];
+  float b[N];
+  float mx = a;
+  #pragma unroll
+  for (int i = 0; i < N; ++i) {
+    b[i] = __ldg(m.lse[i] + h * m.ls[i] + t);
+    mx = fmaxf(mx, b[i]);
+  }
+  if (mx == -INFINITY) {
+    if (final_out) {
+      reinterpret_cast<uint4*>(final_out + off)[0] = make_uint4(0u, 0u, 0u, 0u);
+      reinterpret_cast<uint4*>(final_out + off)[1] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    return;
+  }
+  float o[16];
+  const float w0 = (a == -INFINITY) ? 0.f : __expf(a - mx);
+  float L = w0;
+  if (w0 != 0.f) {
+    #pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 x = reinterpret_cast<const float4*>(ap)[q];
+      o[4 * q] = w0 * x.x; o[4 * q + 1] = w0 * x.y; o[4 * q + 2] = w0 * x.z; o[4 * q + 3] = w0 * x.w;
+    }
+  } else {
+    #pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = 0.f;
+  }
+  #pragma unroll
+  for (int i = 0; i < N; ++i) {
+    if (b[i] == -INFINITY) continue;
+    const float w = __expf(b[i] - mx);
+    L += w;
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(m.blk[i]) + off);
+    const uint4 r0 = __ldg(src), r1 = __ldg(src + 1);
+    const uint32_t wd[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      o[2 * q] = fmaf(w, __uint_as_float(wd[q] << 16), o[2 * q]);
+      o[2 * q + 1] = fmaf(w, __uint_as_float(wd[q] & 0xFFFF0000u), o[2 * q + 1]);
+    }
+  }
+  const float inv = 1.f / L;
+  #pragma unroll
+  for (int k = 0; k < 16; ++k) o[k] *= inv;
+  #pragma unroll
+  for (int q = 0; q < 4; ++q)
+    reinterpret_cast<float4*>(ap)[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+  if (final_out) {
+    uint4* f = reinterpret_cast<uint4*>(final_out + off);
+    f[0] = make_uint4(bf16x2(o[0], o[1]), bf16x2(o[2], o[3]), bf16x2(o[4], o[5]), bf16x2(o[6], o[7]));
+    f[1] = make_uint4(bf16x2(o[8], o[9]), bf16x2(o[10], o[11]), bf16x2(o[12], o[13]),
+                      bf16x2(o[14], o[15]));
+  }
+}
+
 // scalar form (any D, any alignment): one thread per value
 template <typename BT>
 __global__ void merge_n_scalar_kernel(float* acc_out, const float* acc_lse, const __grid_constant__ MergeN m,
@@ -281,8 +359,25 @@ static int merge_n_t(float* acc_out, float* acc_lse, const MergeN& m, int64_t T,
   for (int i = 0; i < m.n; ++i) vec = vec && (reinterpret_cast<uintptr_t>(m.blk[i]) % 16 == 0);
   if (vec) {
     const int64_t threads = T * H * (D / 8);
-    merge_n_vec8_kernel<BT><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-        acc_out, acc_lse, m, T, H, D, als, fin);
+    const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+    bool done = false;
+    if constexpr (std::is_same<BT, __nv_bfloat16>::value) {
+      done = (D % 16 == 0);
+      const unsigned grid16 = static_cast<unsigned>((T * H * (D / 16) + 255) / 256);
+      if (done) switch (m.n) {
+        case 1: merge_n_bf16_kernel<1><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 2: merge_n_bf16_kernel<2><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 3: merge_n_bf16_kernel<3><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 4: merge_n_bf16_kernel<4><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 5: merge_n_bf16_kernel<5><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 6: merge_n_bf16_kernel<6><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 7: merge_n_bf16_kernel<7><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        case 8: merge_n_bf16_kernel<8><<<grid16, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin); break;
+        default: done = false;
+      }
+    }
+    if (!done)
+      merge_n_vec8_kernel<BT><<<grid, 256, 0, s>>>(acc_out, acc_lse, m, T, H, D, als, fin);
   } else {
     const int64_t n = T * H * D;
     merge_n_scalar_kernel<BT><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
