@@ -392,6 +392,7 @@ def run_ours(a):
             transport = "nccl"
     runner = TokenRingAttention(S, H, D, causal=True, record_timeline=True,
                                 transport=transport)
+    runners = [runner]
     q, k, v = rng.local_inputs(a.seed, runner.part, rank, H, D)
     total_flops = causal_flops(S, H, D)
 
@@ -464,9 +465,10 @@ def run_ours(a):
     if not a.no_e2e:
         e2e_steps = max(2, a.steps)     # pipeline fill/drain amortised over the K steps
         groups = next(g for g in (4, 2, 1) if H % g == 0)
-        e2e_ms = e2e_pipelined(
-            lambda hg: TokenRingAttention(S, hg, D, causal=True, transport=transport),
-            q, k, v, e2e_steps, barrier, allmax, groups)
+        def make_runner(hg):
+            runners.append(TokenRingAttention(S, hg, D, causal=True, transport=transport))
+            return runners[-1]
+        e2e_ms = e2e_pipelined(make_runner, q, k, v, e2e_steps, barrier, allmax, groups)
         h2d = 3 * q.numel() * 2 * world
         d2h = (q.numel() * 2 + runner.acc_lse.numel() * 4) * world
         e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
@@ -518,6 +520,9 @@ def run_ours(a):
                           "throughput of the reference's CPU kernels on this host"}
         print(json.dumps(line), flush=True)
     if world > 1:
+        for r in runners:
+            if hasattr(r, "peer"):
+                r.close()
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -330,6 +330,13 @@ class TokenRingAttention:
     def _base(self, call):
         return 2 * self.P + 8 + call * self.P
 
+    def close(self):
+        """Drop the peers' IPC-mapped buffers (call on every rank, then
+        barrier, before the processes exit: a CUDA IPC producer must outlive
+        its consumers' mappings)."""
+        torch.cuda.synchronize(self.device)
+        self.peer = {}
+
     def _flags_of(self, r):
         return self.flags if r == self.rank else self.peer[r][4]
 

@@ -57,6 +57,7 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
             outs.append((res.out.clone(), res.lse.clone()))
         torch.cuda.synchronize()
         q_out.put((rank, [(o.double().cpu().numpy(), l.double().cpu().numpy()) for o, l in outs]))
+        runner.close()
         dist.barrier()
     finally:
         dist.destroy_process_group()
@@ -67,7 +68,8 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
     (2, 1024, 2, 64, False, "ring", "ipc"), (4, 4096, 2, 128, True, "direct", "ipc"),
     (2, 2048, 2, 128, True, "ring", "fused"), (4, 4096, 2, 128, True, "ring", "fused"),
     (3, 3072, 2, 64, False, "ring", "fused"), (4, 4096, 2, 128, True, "direct", "fused"),
-    (3, 1536, 2, 96, True, "ring", "fused")])
+    (3, 1536, 2, 96, True, "ring", "fused"), (8, 8192, 2, 128, True, "ring", "fused"),
+    (8, 8192, 2, 128, True, "direct", "fused")])
 def test_token_ring_ipc(world, S, H, D, causal, route, transport):
     ctx = mp.get_context("spawn")
     q_out = ctx.Queue()
@@ -126,6 +128,7 @@ def _worker_full(rank, world, port, S, H, D, q_out):
             worst_o = max(worst_o, (res.out[l0:l0 + n] - do.float()).abs().max().item())
             worst_l = max(worst_l, (res.lse[:, l0:l0 + n] - dl).abs().max().item())
         q_out.put((rank, worst_o, worst_l))
+        runner.close()
         dist.barrier()
     finally:
         dist.destroy_process_group()
