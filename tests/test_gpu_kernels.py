@@ -261,3 +261,11 @@ def test_merge_n_vs_sequential_oracle(K, d, n, dtype):
     assert np.abs(out - ref_o).max() <= 5e-5
     assert np.all(out[:2] == 0.0)
     assert torch.equal(fin, acc_d.to(torch.bfloat16))
+
+
+def test_enable_peer_access(K):
+    """Same device: a no-op; a device that does not exist: a mapped error, not a crash."""
+    K.enable_peer_access(torch.cuda.current_device())
+    from paper_2412_20501_b200._lib import CudaError, UnsupportedError
+    with pytest.raises((CudaError, UnsupportedError)):
+        K.enable_peer_access(torch.cuda.device_count() + 3)
