@@ -19,7 +19,10 @@ struct AttnCfg {
   static constexpr int NB = D / 64;               // 64-column TMA boxes per tile row
   static constexpr int BOX = 128 * 64 * 2;        // bytes per box (16 KB)
   static constexpr int TILE = NB * BOX;           // bytes per 128-row tile
-  static constexpr int NS = (D == 128) ? 4 : 6;   // kv ring stages (K and V alternate)
+#ifndef TR_NS128
+#define TR_NS128 4
+#endif
+  static constexpr int NS = (D == 128) ? TR_NS128 : 6;   // kv ring stages (K and V alternate)
   static constexpr int THREADS = 384;
   static constexpr int SMEM_TILES = (2 + NS) * TILE;
   static constexpr int SMEM = SMEM_TILES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
