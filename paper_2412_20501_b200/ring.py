@@ -30,7 +30,8 @@ import torch.distributed as dist
 
 from . import kernels
 from .core import Partial
-from .engine import MsgKind, build_token_ring, build_zigzag_token_ring, group_computes
+from .engine import (MsgKind, build_hybrid, build_token_ring, build_zigzag_token_ring,
+                     group_computes)
 from .errors import ConfigError, DimensionError, ScheduleError
 
 
@@ -77,6 +78,11 @@ class RankStep:
     recv_q: list             # [(src, ids)]  union (start order) = next step's buffer layout
     send_out: tuple | None   # (dst, ids)   rows from the previous step's output
     recv_out: list           # [(src, ids)]  to merge after this step's comm
+    # KV residency (hybrid schedules rotate KV across nodes, ref engine.py:233-290):
+    kv_layout: tuple = ()    # kv chunk ids of the store this step reads, in row order
+    kv_store: int = -1       # -1: the local shard; k >= 0: the k-th received KV block
+    send_kv: tuple | None = None   # (dst, ids) of the store, sent after this step
+    recv_kv: tuple | None = None   # (src, ids) received during this step
 
 
 def compile_rank(sched, rank: int) -> list:
@@ -86,6 +92,7 @@ def compile_rank(sched, rank: int) -> list:
     home = tuple(c.id for c in sorted((c for c in sched.chunks if c.home == rank),
                                       key=lambda c: c.start))
     layout = home
+    kv_layout, kv_store, n_kv_recv = home, -1, 0
     start = {c.id: c.start for c in sched.chunks}
     prog = []
     for i, plan in enumerate(plans):
@@ -93,7 +100,7 @@ def compile_rank(sched, rank: int) -> list:
         if g is None:
             raise ScheduleError(f"step {i} rank {rank}: compute set not expressible as one launch")
         q_ids, kv_ids, acc = g
-        send_q, recv_q, send_out = [], [], None
+        send_q, recv_q, send_out, send_kv, recv_kv = [], [], None, None, None
         for m in plan.sends[rank]:
             if m.kind is MsgKind.Q_BLOCK:
                 ids = tuple(m.chunk_ids)
@@ -106,7 +113,10 @@ def compile_rank(sched, rank: int) -> list:
             elif m.kind is MsgKind.OUT_LSE:
                 send_out = (m.dst, tuple(m.chunk_ids))
             else:
-                raise ScheduleError("KV_BLOCK messages are not part of a token-ring program")
+                ids = tuple(m.chunk_ids)
+                if send_kv is not None or not all(b in kv_layout for b in ids):
+                    raise ScheduleError(f"step {i} rank {rank}: cannot send kv chunks {ids}")
+                send_kv = (m.dst, ids)
         recv_out = []
         for src in range(P):
             for m in plan.sends[src]:
@@ -116,12 +126,24 @@ def compile_rank(sched, rank: int) -> list:
                     recv_q.append((src, tuple(m.chunk_ids)))
                 elif m.kind is MsgKind.OUT_LSE:
                     recv_out.append((src, tuple(m.chunk_ids)))
+                else:
+                    if recv_kv is not None:
+                        raise ScheduleError(f"step {i} rank {rank}: two kv blocks in one step")
+                    recv_kv = (src, tuple(m.chunk_ids))
         for a in q_ids:
             if a not in layout:
                 raise ScheduleError(f"step {i} rank {rank}: q chunk {a} not resident")
-        prog.append(RankStep(i, layout, q_ids, kv_ids, acc, send_q, recv_q, send_out, recv_out))
+        for b in kv_ids:
+            if b not in kv_layout:
+                raise ScheduleError(f"step {i} rank {rank}: kv chunk {b} not resident")
+        prog.append(RankStep(i, layout, q_ids, kv_ids, acc, send_q, recv_q, send_out, recv_out,
+                             kv_layout, kv_store, send_kv, recv_kv))
         if recv_q:
             layout = tuple(sorted((a for _, ids in recv_q for a in ids), key=start.get))
+        if recv_kv is not None:
+            if send_kv is None:
+                raise ScheduleError(f"step {i} rank {rank}: kv received without handing one on")
+            kv_layout, kv_store, n_kv_recv = recv_kv[1], n_kv_recv, n_kv_recv + 1
     return prog
 
 
@@ -190,13 +212,21 @@ class TokenRingAttention:
     """
 
     def __init__(self, seq_len, heads, head_dim, causal=True, group=None, ops=None,
-                 device=None, record_timeline=False, transport="nccl", route="ring"):
+                 device=None, record_timeline=False, transport="nccl", route="ring", nodes=1):
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         if route != "ring" and not causal:
             raise ConfigError("route='direct' applies to the causal zigzag schedule only")
-        if causal:
+        if nodes > 1:
+            # the reference's multi-node schedule (ref engine.py:298-303): TokenRing
+            # inside each group of P/nodes ranks, KV rotated across the groups
+            if causal:
+                raise ConfigError("hybrid schedule requires causal=False (ref engine.py:298-303)")
+            if self.P % nodes:
+                raise ConfigError(f"world size {self.P} is not a multiple of nodes={nodes}")
+            self.sched = build_hybrid(nodes, self.P // nodes, seq_len, heads, head_dim)
+        elif causal:
             self.sched = build_zigzag_token_ring(self.P, seq_len, heads, head_dim, route=route)
         else:
             self.sched = build_token_ring(self.P, seq_len, heads, head_dim)
@@ -206,6 +236,8 @@ class TokenRingAttention:
         self.local_rows = self.part.owned_tokens(self.rank)
         self.c = self.sched.chunks[0].tokens
         self.prog = compile_rank(self.sched, self.rank)
+        self.has_kv = any(st.recv_kv is not None for st in self.prog)
+        self._progs = {self.rank: self.prog}
         self._layouts = {}
         # Step 0 computes every home chunk with accumulate=True (TokenRing and
         # zigzag TokenRing alike): those rows are the accumulator's first
@@ -246,6 +278,11 @@ class TokenRingAttention:
         self.acc_out = torch.empty((rows, H, D), dtype=torch.float32, device=dev)
         self.acc_lse = torch.empty((H, rows), dtype=torch.float32, device=dev)
         self.slots = []
+        # received KV blocks (hybrid schedules): two stores, the k-th receive
+        # lands in kvbuf[k % 2]
+        self.kvbuf = ([(torch.empty((rows, H, D), dtype=bf, device=dev),
+                        torch.empty((rows, H, D), dtype=bf, device=dev)) for _ in range(2)]
+                      if self.has_kv else [])
         if self.transport == "fused":
             # one receive slot per message of a forward (bf16 rows + lse), all
             # folded by one n-way merge at the end; and the launch counter the
@@ -279,7 +316,8 @@ class TokenRingAttention:
     # send is a cudaMemcpyAsync straight into the peer's buffer on this rank's
     # copy stream -- copy engines, no SMs taken from the attention kernel --
     # followed by a release store to the peer's sequence flag.
-    # Values are call-relative: call n uses base_n = BASE0 + n*P and every flag
+    # Values are call-relative: call n uses base_n = BASE0 + n*L (L = steps of
+    # the rank program) and every flag
     # only grows, so consecutive calls need no reset, no device sync and no
     # barrier -- each flag's value at the end of call n is exactly its initial
     # condition for call n+1 (set once for call 0 in _ipc_setup).
@@ -287,7 +325,8 @@ class TokenRingAttention:
     #                      folded (fused: a sender may reuse my slots)
     #   flags[1] q_free  : highest step whose traveling-Q slot I am done with
     #   flags[2] o_ready : highest step whose returned OUT for me has landed
-    #   flags[3] o_free  : highest step whose returned OUT I have merged
+    #   flags[3] o_free  : step of the last returned OUT I have merged (base+1:
+    #                      none yet this call, and the previous call's are)
     #   flags[4+s] q_ready from s: highest step whose Q from rank s has landed
     #              (one per source: the direct route has two Q senders per step)
     # fused transport (OUT pushed by the attention epilogue) adds
@@ -295,11 +334,14 @@ class TokenRingAttention:
     #                  last CTA); slot s's buffers are shared as entries 5+2s, 6+2s
     def _ipc_setup(self):
         from torch.multiprocessing.reductions import reduce_tensor
-        self.flags = torch.zeros(4 + self.P + len(self.prog) + 1, dtype=torch.int64,
-                                 device=self.device)
+        # ... flags[KVF] kv_ready: highest step whose KV block for me has landed
+        self.KVF = 4 + self.P + len(self.prog) + 1
+        self.flags = torch.zeros(self.KVF + 1, dtype=torch.int64, device=self.device)
         shared = [self.qbuf[0], self.qbuf[1], self.out_recv, self.lse_recv, self.flags]
         for o, l in self.slots:
             shared += [o, l]
+        for kb, vb in self.kvbuf:          # entries after the slots (see _peer_kv)
+            shared += [kb, vb]
         mine = [reduce_tensor(t) for t in shared]
         everyone = [None] * self.P
         dist.all_gather_object(everyone, mine, group=self.group)
@@ -320,7 +362,7 @@ class TokenRingAttention:
         # initial conditions of call 0, visible to every peer before anyone sends
         b = self._base(0)
         init = torch.full_like(self.flags, b - 1)
-        init[0] = b - self.P            # "the call before 0" has been folded
+        init[0] = b - len(self.prog)    # "the call before 0" has been folded
         init[1] = b                     # step 0 runs on q_loc: slot 0 is free
         init[3] = b + 1                 # ipc: my single OUT receive buffer is free
         self.flags.copy_(init)
@@ -328,7 +370,9 @@ class TokenRingAttention:
         dist.barrier(group=self.group)
 
     def _base(self, call):
-        return 2 * self.P + 8 + call * self.P
+        # call n's flag values live in [base_n - 1, base_n + L + 1], L = steps per call
+        L = len(self.prog)
+        return 2 * L + 8 + call * L
 
     def close(self):
         """Drop the peers' IPC-mapped buffers (call on every rank, then
@@ -336,6 +380,32 @@ class TokenRingAttention:
         its consumers' mappings)."""
         torch.cuda.synchronize(self.device)
         self.peer = {}
+
+    def progs(self, r):
+        """Rank r's step program (compiled on demand; peers' slot indices)."""
+        if r not in self._progs:
+            self._progs[r] = compile_rank(self.sched, r)
+        return self._progs[r]
+
+    def _kv_store(self, st, k_loc, v_loc):
+        """(k, v, layout, local) of the KV store step ``st`` reads."""
+        if st.kv_store < 0:
+            return k_loc, v_loc, st.kv_layout, True
+        kb, vb = self.kvbuf[st.kv_store % 2]
+        return kb, vb, st.kv_layout, False
+
+    def _kv_segs(self, st, local):
+        c = self.c
+        if local:
+            return [(self.part.local_offset(self.rank, self.sched.chunks[b].start), c,
+                     self.sched.chunks[b].start) for b in st.kv_ids]
+        return [(st.kv_layout.index(b) * c, c, self.sched.chunks[b].start) for b in st.kv_ids]
+
+    def _peer_kv(self, r, slot):
+        """Peer r's received-KV store ``slot`` (IPC-mapped)."""
+        nslots = len(self.fplans[r].recv) if self.fplans else 0
+        i0 = 5 + 2 * nslots + 2 * slot
+        return self.peer[r][i0], self.peer[r][i0 + 1]
 
     def _flags_of(self, r):
         return self.flags if r == self.rank else self.peer[r][4]
@@ -382,6 +452,8 @@ class TokenRingAttention:
                     kernels.flag_wait_(self.flags[4 + src:5 + src], base + i, cur)
             if i >= 1 and self.prog[i - 1].recv_out and not fused:
                 kernels.flag_wait_(self.flags[2:3], base + i - 1, cur)
+            if i >= 1 and self.prog[i - 1].recv_kv is not None:        # KV for this phase
+                kernels.flag_wait_(self.flags[self.KVF:self.KVF + 1], base + i, cur)
             if self.record_timeline:
                 ev["comm_ready"] = self.ops.event()
                 self.ops.record(ev["comm_ready"])
@@ -393,10 +465,23 @@ class TokenRingAttention:
                                       self.lse_recv.view(-1)[: H * n].view(H, n)), local_layout)
                 kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
             cur_q = self.qbuf[i % 2] if i > 0 else q_loc
+            kst, vst, kv_lay, kv_local = self._kv_store(st, k_loc, v_loc)
             ev_q = torch.cuda.Event()
             ev_q.record(cur)
-            if st.send_q:
+            if st.send_q or st.send_kv is not None:
                 cs.wait_event(ev_q)
+            if st.send_kv is not None:
+                # hand this phase's KV to the next node's rank (ref engine.py:287-290),
+                # into its receive store once it has finished the previous step
+                dst, ids = st.send_kv
+                a, b = _rows(kv_lay, ids, c)
+                slot = sum(1 for t in self.progs(dst)[:i] if t.recv_kv is not None) % 2
+                pk, pv = self._peer_kv(dst, slot)
+                kernels.flag_wait_(self.peer[dst][4][1:2], base + i - 1, cs)
+                with self._timed_copy(ev, "kv_copies", cs, 2 * (b - a) * H * self.D * 2):
+                    kernels.copy_(pk[: b - a], kst[a:b], cs)
+                    kernels.copy_(pv[: b - a], vst[a:b], cs)
+                kernels.flag_set_(self.peer[dst][4][self.KVF:self.KVF + 1], base + i + 1, cs)
             for dst, ids, from_home in st.send_q:
                 src_buf, src_layout = (q_loc, local_layout) if from_home else (cur_q, st.q_layout)
                 a, b = _rows(src_layout, ids, c)
@@ -409,7 +494,11 @@ class TokenRingAttention:
                 dst, ids = st.send_out
                 a, b = _rows(self.prog[i - 1].q_layout, ids, c)
                 cs.wait_event(ev_comp[i - 1])
-                kernels.flag_wait_(self.peer[dst][4][3:4], base + i - 1, cs)   # home buffer free
+                # the home's single receive buffer is free once it has merged the
+                # previous message it received (messages need not come every step:
+                # the hybrid schedule skips the accumulate steps)
+                prev = [t.step for t in self.progs(dst)[:i] if t.recv_out]
+                kernels.flag_wait_(self.peer[dst][4][3:4], base + (prev[-1] if prev else 1), cs)
                 ob, lb = self.obuf[(i - 1) % 2], self.lbuf[(i - 1) % 2]
                 ls = self.lse_send.view(-1)[: self.H * (b - a)].view(self.H, b - a)
                 with torch.cuda.stream(cs):
@@ -425,14 +514,13 @@ class TokenRingAttention:
                     cur.wait_event(ev_out_sent[i - 1])
                 q_segs = [(_rows(st.q_layout, (a,), c)[0], c, self.sched.chunks[a].start)
                           for a in st.q_ids]
-                kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
-                            self.sched.chunks[b].start) for b in st.kv_ids]
+                kv_segs = self._kv_segs(st, kv_local)
                 buf = i % 2
                 if self.record_timeline:
                     ev["attn_start"] = self.ops.event()
                     self.ops.record(ev["attn_start"])
                 if i == 0 and self.direct_first:
-                    self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                    self.ops.attention(cur_q, kst, vst, q_segs, kv_segs, self.causal,
                                        self.acc_out, self.acc_lse)
                 elif fused and i in fp.push:
                     # compute + send in one kernel: rows go straight into the
@@ -442,16 +530,16 @@ class TokenRingAttention:
                     # merge of it finished before this call's barrier)
                     k, dst, a, b = fp.push[i]
                     # the home has folded the previous call's messages out of its slots
-                    kernels.flag_wait_(self._flags_of(dst)[0:1], base - P, cur)
+                    kernels.flag_wait_(self._flags_of(dst)[0:1], base - len(self.prog), cur)
                     slot = self.fplans[dst].slot_of(k)
                     ob, lb = self._recv_slot(slot, dst)
                     ev["o_push_bytes"] = (b - a) * H * (2 * self.D + 4)   # carried by this launch
                     o = O0 + slot
                     kernels.attention_segments_push(
-                        cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal, ob, lb, a,
+                        cur_q, kst, vst, q_segs, kv_segs, self.causal, ob, lb, a,
                         self.done_count, self._flags_of(dst)[o:o + 1], base + k)
                 else:
-                    self.ops.attention(cur_q, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                    self.ops.attention(cur_q, kst, vst, q_segs, kv_segs, self.causal,
                                        self.obuf[buf], self.lbuf[buf])
                 if self.record_timeline:
                     ev["attn_end"] = self.ops.event()
@@ -469,11 +557,11 @@ class TokenRingAttention:
                 ev["computed"] = self.ops.event()
                 self.ops.record(ev["computed"])
                 self.timeline.append(ev)
-            if i < P:
-                # my traveling-Q slot i%2 is free once both this step's compute
-                # and my own forward copy of it are done
-                cs.wait_event(ev_comp[i])
-                kernels.flag_set_(self.flags[1:2], base + i, cs)
+            # step i is done here: my traveling-Q slot i%2 (and, in hybrid
+            # schedules, the KV store read before this step) is free once
+            # this step's compute and my own forward copies are done
+            cs.wait_event(ev_comp[i])
+            kernels.flag_set_(self.flags[1:2], base + i, cs)
         last = self.prog[-1]
         if fused:
             self._merge_all_fused(base, cur, local_layout)
@@ -486,10 +574,11 @@ class TokenRingAttention:
         # hand the next call its initial conditions (next base = base + P):
         # everything received is folded, the OUT buffer is free, and both
         # traveling-Q slots are free once this call's computes are done
+        L = len(self.prog)
         kernels.flag_set_(self.flags[0:1], base, cur)
-        kernels.flag_set_(self.flags[3:4], base + P + 1, cur)
+        kernels.flag_set_(self.flags[3:4], base + L + 1, cur)
         cs.wait_stream(cur)
-        kernels.flag_set_(self.flags[1:2], base + P, cs)
+        kernels.flag_set_(self.flags[1:2], base + L, cs)
         cur.wait_stream(cs)
         return Partial(self.acc_out, self.acc_lse)
 
@@ -551,6 +640,7 @@ class TokenRingAttention:
                 self._merge_returned(pending_out, local_layout)
             sends, recvs = [], []
             cur = self.qbuf[i % 2] if i > 0 else q_loc
+            kst, vst, kv_lay, kv_local = self._kv_store(st, k_loc, v_loc)
             for dst, ids, from_home in st.send_q:
                 src_buf, src_layout = (q_loc, local_layout) if from_home else (cur, st.q_layout)
                 a, b = _rows(src_layout, ids, c)
@@ -577,20 +667,28 @@ class TokenRingAttention:
                 recvs.append((src, self.out_recv[:n]))
                 recvs.append((src, lr))
                 pending_out = (ids, self.out_recv[:n], lr)
+            if st.send_kv is not None:          # hybrid: KV to the next node's rank
+                a, b = _rows(kv_lay, st.send_kv[1], c)
+                sends.append((st.send_kv[0], kst[a:b]))
+                sends.append((st.send_kv[0], vst[a:b]))
+            if st.recv_kv is not None:
+                kb, vb = self.kvbuf[self.prog[i + 1].kv_store % 2]
+                n = len(st.recv_kv[1]) * c
+                recvs.append((st.recv_kv[0], kb[:n]))
+                recvs.append((st.recv_kv[0], vb[:n]))
             pending = self._comm(sends, recvs)
             if st.q_ids:
                 q_segs = []
                 for a in st.q_ids:
                     r0, _ = _rows(st.q_layout, (a,), c)
                     q_segs.append((r0, c, self.sched.chunks[a].start))
-                kv_segs = [(self.part.local_offset(rank, self.sched.chunks[b].start), c,
-                            self.sched.chunks[b].start) for b in st.kv_ids]
+                kv_segs = self._kv_segs(st, kv_local)
                 buf = i % 2
                 if self.record_timeline:
                     ev["attn_start"] = self.ops.event()
                     self.ops.record(ev["attn_start"])
                 first = i == 0 and self.direct_first
-                self.ops.attention(cur, k_loc, v_loc, q_segs, kv_segs, self.causal,
+                self.ops.attention(cur, kst, vst, q_segs, kv_segs, self.causal,
                                    self.acc_out if first else self.obuf[buf],
                                    self.acc_lse if first else self.lbuf[buf])
                 if self.record_timeline:

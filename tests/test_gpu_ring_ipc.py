@@ -23,6 +23,18 @@ from oracle import splitmix
 pytestmark = pytest.mark.gpu
 
 
+_reap = []     # workers of the current test; killed if a test fails mid-way
+
+
+@pytest.fixture(autouse=True)
+def _kill_workers():
+    yield
+    while _reap:
+        p = _reap.pop()
+        if p.is_alive():
+            p.kill()
+
+
 def _port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -34,7 +46,7 @@ def _port():
 SEEDS = (21, 22, 21)
 
 
-def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
+def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, nodes=1):
     """Back-to-back calls with different inputs and no host synchronisation
     in between (the runner's flags carry each call's initial conditions);
     rank 0 is delayed on the device before every call so its peers run ahead
@@ -47,7 +59,7 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
         from paper_2412_20501_b200 import rng
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
-                                    transport=transport, route=route)
+                                    transport=transport, route=route, nodes=nodes)
         inputs = {sd: rng.local_inputs(sd, runner.part, rank, H, D) for sd in set(SEEDS)}
         outs = []
         for sd in SEEDS[:calls]:
@@ -69,16 +81,22 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport):
     (2, 2048, 2, 128, True, "ring", "fused"), (4, 4096, 2, 128, True, "ring", "fused"),
     (3, 3072, 2, 64, False, "ring", "fused"), (4, 4096, 2, 128, True, "direct", "fused"),
     (3, 1536, 2, 96, True, "ring", "fused"), (8, 8192, 2, 128, True, "ring", "fused"),
-    (8, 8192, 2, 128, True, "direct", "fused")])
+    (8, 8192, 2, 128, True, "direct", "fused"),
+    # the multi-node hybrid schedule (KV rotated across "nodes" of 2 ranks)
+    (4, 2048, 2, 128, False, "hybrid2", "ipc"), (4, 2048, 2, 128, False, "hybrid2", "fused"),
+    (6, 3072, 2, 64, False, "hybrid3", "fused")])
 def test_token_ring_ipc(world, S, H, D, causal, route, transport):
     ctx = mp.get_context("spawn")
     q_out = ctx.Queue()
     port = _port()
+    nodes = int(route[6:]) if route.startswith("hybrid") else 1
+    route = "ring" if nodes > 1 else route
     procs = [ctx.Process(target=_worker,
-                         args=(r, world, port, S, H, D, causal, 3, q_out, route, transport))
+                         args=(r, world, port, S, H, D, causal, 3, q_out, route, transport, nodes))
              for r in range(world)]
     for p in procs:
         p.start()
+    _reap.extend(procs)
     res = {}
     for _ in range(world):
         r, calls_out = q_out.get(timeout=300)
@@ -86,7 +104,10 @@ def test_token_ring_ipc(world, S, H, D, causal, route, transport):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    sched = osch.zigzag_token_ring(world, S, H, D) if causal else osch.token_ring(world, S, H, D)
+    if nodes > 1:
+        sched = osch.hybrid(nodes, world // nodes, S, H, D)
+    else:
+        sched = osch.zigzag_token_ring(world, S, H, D) if causal else osch.token_ring(world, S, H, D)
     refs = {}
     for sd in set(SEEDS):
         q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(sd, S, H, D))
@@ -147,6 +168,7 @@ def test_fused_full_size_vs_dense_launch(world):
              for r in range(world)]
     for p in procs:
         p.start()
+    _reap.extend(procs)
     got = [q_out.get(timeout=600) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)

@@ -19,6 +19,18 @@ from oracle import schedule as osch
 from oracle import splitmix
 
 
+_reap = []     # workers of the current test; killed if a test fails mid-way
+
+
+@pytest.fixture(autouse=True)
+def _kill_workers():
+    yield
+    while _reap:
+        p = _reap.pop()
+        if p.is_alive():
+            p.kill()
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -27,7 +39,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring"):
+def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring", nodes=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -35,7 +47,7 @@ def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring"):
         from cpu_ops import OracleOps
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, ops=OracleOps(), device="cpu",
-                                    route=route)
+                                    route=route, nodes=nodes)
         q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(seed, S, H, D))
         rng = runner.part.ranges(rank)
         loc = [torch.as_tensor(opart.gather(x, rng), dtype=torch.float32).to(torch.bfloat16)
@@ -59,6 +71,7 @@ def test_token_ring_gloo(world, S, H, D, causal, route):
              for r in range(world)]
     for p in procs:
         p.start()
+    _reap.extend(procs)
     res = {}
     for _ in range(world):
         r, o, l = q_.get(timeout=120)
@@ -78,4 +91,40 @@ def test_token_ring_gloo(world, S, H, D, causal, route):
     g_out, g_lse = opart.reorder([res[r][0] for r in range(world)],
                                  [res[r][1] for r in range(world)], osch.ranges_of(sched, S), S)
     d_out, d_lse = ok.dense_attention(q, k, v, causal)
+    assert ok.max_relative_error(g_out, g_lse, d_out, d_lse) <= 2e-2
+
+
+@pytest.mark.parametrize("nodes,per_node,S", [(2, 2, 64), (2, 3, 96), (3, 2, 96)])
+def test_hybrid_gloo(nodes, per_node, S):
+    """The reference's multi-node schedule (TokenRing inside a node, KV
+    rotated across nodes; ref engine.py:233-303) run by the multi-process
+    runner: KV blocks travel at the hand-off steps into the receiver's second
+    KV store, per rank the result equals the oracle's execute of the same
+    schedule, and the whole equals dense non-causal attention."""
+    world, H, D = nodes * per_node, 2, 8
+    ctx = mp.get_context("spawn")
+    q_ = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, S, H, D, False, 13, q_, "ring", nodes))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    _reap.extend(procs)
+    res = {}
+    for _ in range(world):
+        r, o, l = q_.get(timeout=120)
+        res[r] = (o, l)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(13, S, H, D))
+    sched = osch.hybrid(nodes, per_node, S, H, D)
+    ref = osch.execute(sched, q, k, v)
+    for r in range(world):
+        assert np.abs(res[r][0] - ref[r][0]).max() <= 2e-2
+        assert np.abs(res[r][1] - ref[r][1]).max() <= 1e-3
+    g_out, g_lse = opart.reorder([res[r][0] for r in range(world)],
+                                 [res[r][1] for r in range(world)], osch.ranges_of(sched, S), S)
+    d_out, d_lse = ok.dense_attention(q, k, v, False)
     assert ok.max_relative_error(g_out, g_lse, d_out, d_lse) <= 2e-2
