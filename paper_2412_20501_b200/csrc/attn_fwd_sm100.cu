@@ -246,41 +246,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       uint32_t s[128];
       // masking is decided per 128-row half (uniform across the warpgroup)
       const bool need_mask = valid < 128 || (p.causal && kpos + 127 > half_min_pos);
-#ifdef TR_SPLIT_SLOAD
-      // experiment: reduce the first 64 columns while the last 64 are loading
-      tmem_ld32_at<0>(tS + 0, s);
-      tmem_ld32_at<32>(tS + 32, s);
-      tc_wait_ld();
-      tmem_ld32_at<64>(tS + 64, s);
-      tmem_ld32_at<96>(tS + 96, s);
-      int limit_ = 128;
-      if (need_mask) {
-        int64_t lim = valid;
-        if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
-        limit_ = static_cast<int>(imax64(lim, 0));
-        #pragma unroll
-        for (int i = 0; i < 64; ++i) s[i] = (i < limit_) ? s[i] : 0xFF800000u;
-      }
-      float mxa = __uint_as_float(s[0]), mxa2 = __uint_as_float(s[1]);
-      #pragma unroll
-      for (int i = 2; i < 64; i += 4) {
-        mxa = fmaxf(mxa, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
-        mxa2 = fmaxf(mxa2, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
-      }
-      tc_wait_ld();
-      reg_fence<64>(s);                 // no use of s[64..127] before the wait
-      if (need_mask) {
-        #pragma unroll
-        for (int i = 64; i < 128; ++i) s[i] = (i < limit_) ? s[i] : 0xFF800000u;
-      }
-      float mx = __uint_as_float(s[64]), mxb = __uint_as_float(s[65]);
-      #pragma unroll
-      for (int i = 66; i < 128; i += 4) {
-        mx = fmaxf(mx, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
-        mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
-      }
-      mx = fmaxf(fmaxf(mx, mxb), fmaxf(mxa, mxa2));
-#else
       tmem_ld32_at<0>(tS + 0, s);
       tmem_ld32_at<32>(tS + 32, s);
       tmem_ld32_at<64>(tS + 64, s);
@@ -293,19 +258,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         #pragma unroll
         for (int i = 0; i < 128; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;  // -inf
       }
-#if defined(TR_MAX_CHAINS) && TR_MAX_CHAINS == 4
-      // four independent 3-input max chains (16 deep instead of 32)
-      float m4[4];
-      #pragma unroll
-      for (int u = 0; u < 4; ++u) m4[u] = fmaxf(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1]));
-      #pragma unroll
-      for (int i = 8; i < 128; i += 8) {
-        #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          m4[u] = fmaxf(m4[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
-      }
-      float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-#else
       float mx = __uint_as_float(s[0]);
       float mxb = __uint_as_float(s[1]);
       #pragma unroll
@@ -314,8 +266,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
       }
       mx = fmaxf(mx, mxb);
-#endif
-#endif  // TR_SPLIT_SLOAD
       TR_TRACE_AT(2, j);
       const bool grow = mx > m_used + thresh;
       const bool scale_o = grow && m_used != -INFINITY;

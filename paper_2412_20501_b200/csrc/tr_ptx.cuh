@@ -358,29 +358,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       : "memory");
 }
 
-// Register fence: an empty asm that "modifies" registers [OFF, OFF+32) of r,
-// so no use of them can be scheduled before this point (e.g. before the
-// tcgen05.wait::ld that completes an asynchronous TMEM load into them).
-template <int OFF, int N>
-__device__ __forceinline__ void reg_fence32(uint32_t (&r)[N]) {
-  asm volatile(""
-               : "+r"(r[OFF + 0]), "+r"(r[OFF + 1]), "+r"(r[OFF + 2]), "+r"(r[OFF + 3]),
-                 "+r"(r[OFF + 4]), "+r"(r[OFF + 5]), "+r"(r[OFF + 6]), "+r"(r[OFF + 7]),
-                 "+r"(r[OFF + 8]), "+r"(r[OFF + 9]), "+r"(r[OFF + 10]), "+r"(r[OFF + 11]),
-                 "+r"(r[OFF + 12]), "+r"(r[OFF + 13]), "+r"(r[OFF + 14]), "+r"(r[OFF + 15]));
-  asm volatile(""
-               : "+r"(r[OFF + 16]), "+r"(r[OFF + 17]), "+r"(r[OFF + 18]), "+r"(r[OFF + 19]),
-                 "+r"(r[OFF + 20]), "+r"(r[OFF + 21]), "+r"(r[OFF + 22]), "+r"(r[OFF + 23]),
-                 "+r"(r[OFF + 24]), "+r"(r[OFF + 25]), "+r"(r[OFF + 26]), "+r"(r[OFF + 27]),
-                 "+r"(r[OFF + 28]), "+r"(r[OFF + 29]), "+r"(r[OFF + 30]), "+r"(r[OFF + 31]));
-}
-// 64 registers [OFF, OFF+64)
-template <int OFF, int N>
-__device__ __forceinline__ void reg_fence(uint32_t (&r)[N]) {
-  reg_fence32<OFF>(r);
-  reg_fence32<OFF + 32>(r);
-}
-
 // ---------------------------------------------------------------- registers
 template <uint32_t N>
 __device__ __forceinline__ void setmaxnreg_inc() {
