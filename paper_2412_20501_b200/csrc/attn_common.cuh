@@ -24,11 +24,8 @@ struct AttnCfg {
 #endif
   static constexpr int NS = (D == 128) ? TR_NS128 : 6;   // kv ring stages (K and V alternate)
   static constexpr int THREADS = 384;
-  static constexpr int THREADS_SPLIT = 640;       // split-row softmax: 16 softmax warps
   static constexpr int SMEM_TILES = (2 + NS) * TILE;
   static constexpr int SMEM = SMEM_TILES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
-  static constexpr int XCHG = 3 * 512 * 4;        // split-row max (2 buffers) + row-sum exchange
-  static constexpr int SMEM_SPLIT = SMEM + XCHG;
   static constexpr uint32_t IDESC_QK = idesc_bf16(128, BN, false);
   static constexpr uint32_t IDESC_PV = idesc_bf16(128, D, true);
   static constexpr float RESCALE_LOG2 = 8.0f;
@@ -56,12 +53,12 @@ struct AttnCfg {
 static __device__ unsigned long long g_trace[2 * 12 * 64 * 8];
 #define TR_TRACE_AT(slot, jj)                                                        \
   do {                                                                               \
-    if (blockIdx.x < 2 && warp < 12 && lane == 0 && (jj) < 64)                                  \
+    if (blockIdx.x < 2 && lane == 0 && (jj) < 64)                                    \
       g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = clock64();      \
   } while (0)
 #define TR_TRACE_GT(slot, jj)                                                        \
   do {                                                                               \
-    if (blockIdx.x < 2 && warp < 12 && lane == 0 && (jj) < 64)                                  \
+    if (blockIdx.x < 2 && lane == 0 && (jj) < 64)                                    \
       g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = globaltimer_ns(); \
   } while (0)
 #else
@@ -157,35 +154,6 @@ __device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, ui
     tc_fence_before();
     mbar_arrive(&pbar[kh]);
   }
-}
-
-// Split-row form (attn_fwd_sm100_kernel<D, true>): exp2 of the 64 scores of
-// one key group -> 32 packed bf16x2 TMEM columns at tP, row sums in lsum2,
-// one arrival on pbar once the chunk is in TMEM.
-template <int POLY_MOD, bool kPoly>
-__device__ __forceinline__ void emit_p64(const uint32_t (&s)[64], uint32_t tP, uint64_t c2,
-                                         uint64_t nmc2, uint64_t (&lsum2)[2], uint64_t* pbar) {
-  uint32_t pk[32];
-  #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const uint64_t x2 =
-        ffma2(f2pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nmc2);
-    float a, b;
-    f2unpack(x2, a, b);
-    uint64_t p2;
-    if (kPoly && (i % POLY_MOD) == POLY_MOD - 1)
-      p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f)));
-    else
-      p2 = f2pack(ex2_approx(a), ex2_approx(b));
-    lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
-    float pa, pb;
-    f2unpack(p2, pa, pb);
-    pk[i] = pack_bf16x2(pa, pb);
-  }
-  tmem_st32(tP, pk);
-  tc_wait_st();
-  tc_fence_before();
-  mbar_arrive(pbar);
 }
 
 // ------------------------------------------------------------------ host hooks

@@ -28,170 +28,10 @@
 
 #include "attn_common.cuh"
 
-#ifndef TR_SPLIT_DEFAULT
-#define TR_SPLIT_DEFAULT 0
-#endif
-
 namespace tr {
 
-// Split-row softmax + epilogue (attn_fwd_sm100_kernel<D, true>): 16 softmax
-// warps, two per TMEM lane quarter and half, so each thread owns one row's
-// 64 keys of every tile (key group g) and half of its O columns.  With one
-// warp per row (the other instantiation) a half's softmax is a single warp
-// per SM sub-partition and its load/max/store phases leave MUFU idle; here
-// two warps feed each sub-partition's MUFU.  The pair of warps sharing rows
-// exchanges the tile's row max through shared memory (named barrier 1+4h+q,
-// 64 threads) -- which also orders group 1's P store (TMEM columns 32..63 of
-// S_h) after group 0's load of those columns -- and the row sums once at the
-// end.  Same online softmax, lazy rescale and P layout as the one-warp form.
 template <int D>
-__device__ __forceinline__ void softmax_split(const AttnPlan& p, const tr_segment& Q, int head,
-                                              int64_t qrow0, int ntiles, const int64_t* kv_tiles,
-                                              uint32_t tmem, uint64_t* s_full, uint64_t* p_full,
-                                              uint64_t* o_done, float* xchg) {
-  using C = AttnCfg<D>;
-  static_assert(C::NPC == 2, "split-row softmax publishes P in two 64-key chunks");
-  const int warp = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  const int idx = warp - 4;
-  const int h = idx / 8;                // which 128-row half
-  const int g = (idx / 4) % 2;          // key group: keys [64g, 64g+64) of every tile
-  const int quarter = warp % 4;         // TMEM lane quarter (= SM sub-partition)
-  const int r = quarter * 32 + lane;    // row inside the half
-  const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-  const uint32_t tS = tmem + lane_base + h * 128;
-  const uint32_t tOg = tmem + lane_base + 256 + h * 128 + g * (D / 2);
-  const uint32_t pair_bar = 1 + 4 * h + quarter;
-  const uint32_t x_me = smem_u32(xchg + (h * 2 + g) * 128 + r);   // + parity * 2048 bytes
-  const uint32_t x_peer = smem_u32(xchg + (h * 2 + 1 - g) * 128 + r);
-  const int64_t row_in_seg = qrow0 + 128 * h + r;
-  const int64_t my_pos = Q.pos0 + row_in_seg;
-  const int64_t half_min_pos = Q.pos0 + qrow0 + 128 * h;
-  const float c = p.scale_log2;
-  const float thresh = C::RESCALE_LOG2 / c;
-  const uint64_t c2 = f2pack(c, c);
-  float m_used = -INFINITY;
-  uint64_t lsum2[2] = {0ull, 0ull};
-  KvWalk w = kv_begin(kv_tiles);
-  for (int j = 0; j < ntiles; ++j, w.next(kv_tiles)) {
-    const int64_t kpos = p.kv[w.g].pos0 + w.t * 128 + 64 * g;
-    const int valid = static_cast<int>(imax64(0, imin64(64, p.kv[w.g].rows - w.t * 128 - 64 * g)));
-    mbar_wait(&s_full[h], j & 1);
-    tc_fence_after();
-    uint32_t s[64];
-    tmem_ld32_at<0>(tS + 64 * g, s);
-    tmem_ld32_at<32>(tS + 64 * g + 32, s);
-    tc_wait_ld();
-    const bool need_mask = valid < 64 || (p.causal && kpos + 63 > half_min_pos);
-    if (need_mask) {
-      int64_t lim = valid;
-      if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
-      const int limit = static_cast<int>(imax64(lim, 0));
-      #pragma unroll
-      for (int i = 0; i < 64; ++i) s[i] = (i < limit) ? s[i] : 0xFF800000u;  // -inf
-    }
-    float mx = __uint_as_float(s[0]);
-    float mxb = __uint_as_float(s[1]);
-    #pragma unroll
-    for (int i = 2; i < 62; i += 4) {
-      mx = fmaxf(mx, fmaxf(__uint_as_float(s[i]), __uint_as_float(s[i + 1])));
-      mxb = fmaxf(mxb, fmaxf(__uint_as_float(s[i + 2]), __uint_as_float(s[i + 3])));
-    }
-    mx = fmaxf(fmaxf(mx, __uint_as_float(s[62])), fmaxf(mxb, __uint_as_float(s[63])));
-    const uint32_t par = (j & 1) * 2048u;
-    st_shared_f32(x_me + par, mx);
-    tc_fence_before();                  // my S load is ordered before the peer's P store
-    named_barrier_sync(pair_bar, 64);
-    tc_fence_after();
-    mx = fmaxf(mx, ld_shared_f32(x_peer + par));
-    const bool grow = mx > m_used + thresh;
-    const bool scale_o = grow && m_used != -INFINITY;
-    // both warps of the pair hold the same rows, m_used and mx: same branch
-    if (__any_sync(0xffffffffu, scale_o)) {
-      const float f = scale_o ? ex2_approx((m_used - mx) * c) : 1.f;
-      const uint64_t f2 = f2pack(f, f);
-      lsum2[0] = fmul2(lsum2[0], f2);
-      lsum2[1] = fmul2(lsum2[1], f2);
-      #pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t u[16];
-        tmem_ld16(tOg + cc * 16, u);
-        tc_wait_ld();
-        #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          const uint64_t v = fmul2(f2pack(__uint_as_float(u[i]), __uint_as_float(u[i + 1])), f2);
-          u[i] = static_cast<uint32_t>(v);
-          u[i + 1] = static_cast<uint32_t>(v >> 32);
-        }
-        tmem_st16(tOg + cc * 16, u);
-      }
-      tc_wait_st();
-      tc_fence_before();
-      // neither half of the row publishes P (the P.V MMA writes every O
-      // column) before both halves of O are rescaled
-      named_barrier_sync(pair_bar, 64);
-      tc_fence_after();
-    }
-    if (grow) m_used = mx;
-    const float mc = (m_used == -INFINITY) ? 0.f : m_used * c;
-    const uint64_t nmc2 = f2pack(-mc, -mc);
-    if (need_mask)
-      emit_p64<C::POLY_MOD, false>(s, tS + 32 * g, c2, nmc2, lsum2, &p_full[2 * h + g]);
-    else
-      emit_p64<C::POLY_MOD, true>(s, tS + 32 * g, c2, nmc2, lsum2, &p_full[2 * h + g]);
-  }
-  float l;
-  {
-    float a0, a1, b0, b1;
-    f2unpack(lsum2[0], a0, a1);
-    f2unpack(lsum2[1], b0, b1);
-    l = (a0 + a1) + (b0 + b1);
-  }
-  st_shared_f32(x_me + 4096u, l);
-  named_barrier_sync(pair_bar, 64);
-  l += ld_shared_f32(x_peer + 4096u);
-  // ---------------------------------------------------------- epilogue
-  const bool row_ok = row_in_seg < Q.rows;
-  const int64_t grow_ = Q.row0 + row_in_seg;
-  const int64_t oidx = (grow_ * p.heads + head) * D + g * (D / 2);
-  if (ntiles > 0) {
-    mbar_wait(&o_done[h], 0);
-    tc_fence_after();
-  }
-  const float inv = (l > 0.f) ? 1.f / l : 0.f;
-  #pragma unroll
-  for (int cc = 0; cc < D / 64; ++cc) {
-    uint32_t u[32];
-    if (ntiles > 0) {
-      tmem_ld32(tOg + cc * 32, u);
-      tc_wait_ld();
-    } else {
-      #pragma unroll
-      for (int i = 0; i < 32; ++i) u[i] = 0u;
-    }
-    if (!row_ok) continue;
-    if (p.out_f32) {
-      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + oidx + cc * 32);
-      #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        dst[i] = make_float4(__uint_as_float(u[4 * i]) * inv, __uint_as_float(u[4 * i + 1]) * inv,
-                             __uint_as_float(u[4 * i + 2]) * inv, __uint_as_float(u[4 * i + 3]) * inv);
-      continue;
-    }
-    uint32_t pk[16];
-    #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      pk[i] = pack_bf16x2(__uint_as_float(u[2 * i]) * inv, __uint_as_float(u[2 * i + 1]) * inv);
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.out) + oidx + cc * 32);
-    #pragma unroll
-    for (int i = 0; i < 4; ++i) dst[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-  }
-  if (row_ok && g == 0)
-    p.lse[head * p.lse_stride + grow_] = (l > 0.f) ? (logf(l) + m_used * p.scale) : -INFINITY;
-}
-
-template <int D, bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? 640 : 384, 1)
+__global__ void __launch_bounds__(384, 1)
 attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
                       const __grid_constant__ CUtensorMap tmv, const __grid_constant__ AttnPlan p) {
   using C = AttnCfg<D>;
@@ -208,9 +48,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   uint64_t* o_done = p_full + 2 * C::NPC;       // [2]
   int64_t* kv_tiles = reinterpret_cast<int64_t*>(o_done + 2);  // [4]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 6);
-  // split-row softmax only: [2 tile parities][2 halves][2 key groups][128 rows]
-  // running-max exchange, then [2 halves][2 key groups][128 rows] row sums
-  float* xchg = reinterpret_cast<float*>(smem + C::SMEM_TILES + 1024);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -255,7 +92,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   // Register rebalancing: each role's code sits inside the branch of its own
   // setmaxnreg so ptxas compiles it against that budget.
   if (warp < 4) {
-   setmaxnreg_dec<SPLIT ? 48 : 56>();
+   setmaxnreg_dec<56>();
    if (warp == 0 && ntiles > 0) {
     // ------------------------------------------------------------ producer
     // The whole warp walks the loop (warp-uniform state in uniform
@@ -360,9 +197,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     tc_commit_elect(&kv_empty[prev_v_stage]);
     tc_commit_elect(&o_done[1]);
    }
-  } else if constexpr (SPLIT) {
-   setmaxnreg_inc<104>();
-   softmax_split<D>(p, Q, head, qrow0, ntiles, kv_tiles, tmem, s_full, p_full, o_done, xchg);
   } else {
    setmaxnreg_inc<224>();
    {
@@ -582,34 +416,6 @@ bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const
   return true;
 }
 
-// Split-row softmax (16 softmax warps) on/off; TR_ATTN_SPLIT=0/1 overrides
-// at run time (A/B on the same build)
-static bool split_softmax() {
-  static int v = -1;
-  if (v < 0) {
-    v = TR_SPLIT_DEFAULT;
-    if (const char* e = getenv("TR_ATTN_SPLIT")) v = e[0] == '1';
-  }
-  return v == 1;
-}
-
-template <int D, bool SPLIT>
-static int launch_k(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                    AttnPlan& plan, int64_t blocks, cudaStream_t s) {
-  using C = AttnCfg<D>;
-  constexpr int smem = SPLIT ? C::SMEM_SPLIT : C::SMEM;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, SPLIT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_sm100)");
-    attr_done = true;
-  }
-  attn_fwd_sm100_kernel<D, SPLIT>
-      <<<static_cast<unsigned>(blocks), SPLIT ? C::THREADS_SPLIT : C::THREADS, smem, s>>>(tq, tk, tv, plan);
-  return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
-}
-
 template <int D>
 static int launch_d(const void* q, const void* k, const void* v, int64_t tq_total, int64_t tk_total,
                     AttnPlan& plan, cudaStream_t s) {
@@ -620,14 +426,21 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
   if ((rc = make_tmap(&tq, q, tq_total, row_elems))) return rc;
   if ((rc = make_tmap(&tk, k, tk_total, row_elems))) return rc;
   if ((rc = make_tmap(&tv, v, tk_total, row_elems))) return rc;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_sm100)");
+    attr_done = true;
+  }
   const int64_t blocks = plan.tile_prefix[plan.nq] * plan.heads;
   if (blocks == 0) return TR_OK;
   if (blocks > 0x7FFFFFFF) return fail(TR_ERR_UNSUPPORTED, "grid too large");
   // opt-in measured alternatives (TR_ATTN_PSMEM / TR_ATTN_PERSISTENT)
   const int vrc = launch_attn_variant(tq, tk, tv, plan, D, blocks, s);
   if (vrc != -1) return vrc;
-  return split_softmax() ? launch_k<D, true>(tq, tk, tv, plan, blocks, s)
-                         : launch_k<D, false>(tq, tk, tv, plan, blocks, s);
+  attn_fwd_sm100_kernel<D><<<static_cast<unsigned>(blocks), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
+  return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
 }
 
 
