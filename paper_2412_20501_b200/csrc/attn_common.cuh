@@ -40,12 +40,6 @@ struct AttnCfg {
   // so O += P.V starts on the first chunk while the rest is still exponentiated
   static constexpr int NPC = TR_P_CHUNKS;
   static_assert(NPC == 2 || NPC == 4, "P chunks: 2 or 4");
-#ifndef TR_P_FIRST
-#define TR_P_FIRST 4
-#endif
-  // with two chunks: 16-key P.V steps in the first chunk (4 = even split)
-  static constexpr int P_FIRST = (NPC == 2) ? TR_P_FIRST : 8 / NPC;
-  static_assert(P_FIRST >= 1 && P_FIRST <= 7, "first P chunk: 1..7 sixteen-key steps");
 };
 
 // Per-CTA kv tile walk: the tile count of every kv segment lives in shared
@@ -156,43 +150,6 @@ __device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, ui
     }
     if constexpr (PAIRS == 32) tmem_st32(tS + kh * 32, pk);
     else tmem_st16(tS + kh * 16, pk);
-    tc_wait_st();
-    tc_fence_before();
-    mbar_arrive(&pbar[kh]);
-  }
-}
-
-// Two P chunks of uneven size: the first FIRST*16 keys, then the rest (so the
-// P.V left after the last chunk is short).  Stores in 8-column (16-key) blocks.
-template <int POLY_MOD, bool kPoly, int FIRST>
-__device__ __forceinline__ void emit_p_uneven(const uint32_t (&s)[128], uint32_t tS, uint64_t c2,
-                                              uint64_t nmc2, uint64_t (&lsum2)[2], uint64_t* pbar) {
-  #pragma unroll
-  for (int kh = 0; kh < 2; ++kh) {
-    const int b0 = kh == 0 ? 0 : FIRST;        // 16-column blocks [b0, b1)
-    const int b1 = kh == 0 ? FIRST : 8;
-    #pragma unroll
-    for (int b = b0; b < b1; ++b) {
-      uint32_t pk[8];
-      #pragma unroll
-      for (int ii = 0; ii < 8; ++ii) {
-        const int i = b * 8 + ii;              // pair index in the row
-        const uint64_t x2 =
-            ffma2(f2pack(__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])), c2, nmc2);
-        float a, bb;
-        f2unpack(x2, a, bb);
-        uint64_t p2;
-        if (kPoly && (i % POLY_MOD) == POLY_MOD - 1)
-          p2 = exp2_poly2(f2pack(fmaxf(a, -126.f), fmaxf(bb, -126.f)));
-        else
-          p2 = f2pack(ex2_approx(a), ex2_approx(bb));
-        lsum2[i & 1] = fadd2(lsum2[i & 1], p2);
-        float pa, pb;
-        f2unpack(p2, pa, pb);
-        pk[ii] = pack_bf16x2(pa, pb);
-      }
-      tmem_st8(tS + b * 8, pk);              // 8 pairs = 8 TMEM columns
-    }
     tc_wait_st();
     tc_fence_before();
     mbar_arrive(&pbar[kh]);

@@ -144,11 +144,9 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     constexpr int KPC = 8 / C::NPC;      // 16-key MMA steps per P chunk
     auto pv = [&](int h, int stage, int kh, bool acc) {
       const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
-      // chunk kh covers 16-key steps [k_lo, k_hi) (uneven with TR_P_FIRST)
-      const int k_lo = (C::NPC == 2) ? (kh == 0 ? 0 : C::P_FIRST) : kh * KPC;
-      const int k_hi = (C::NPC == 2) ? (kh == 0 ? C::P_FIRST : 8) : (kh + 1) * KPC;
       #pragma unroll
-      for (int kk = k_lo; kk < k_hi; ++kk) {
+      for (int k4 = 0; k4 < KPC; ++k4) {
+        const int kk = kh * KPC + k4;
 #if defined(TR_EXP_NOSOFTMAX) && defined(TR_EXP_PSMEM)
         // experiment: A (P) from shared memory, SS mode
         const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
@@ -164,11 +162,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     auto pv_both = [&](int h, int stage, uint32_t phase, bool acc) {
       #pragma unroll
       for (int kh = 0; kh < C::NPC; ++kh) {
-#ifdef TR_MMA_WAIT_HINT
-        mbar_wait_hinted(&p_full[C::NPC * h + kh], phase, TR_MMA_WAIT_HINT);
-#else
         mbar_wait(&p_full[C::NPC * h + kh], phase);
-#endif
         tc_fence_after();
         pv(h, stage, kh, acc || kh > 0);
       }
@@ -307,17 +301,10 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       // key halves so the P.V MMA can start on the first half early.  Masked
       // tiles keep every exp2 on MUFU (exact 0 for -inf); full tiles move one
       // pair in POLY_MOD to the FMA pipe.
-      if constexpr (C::NPC == 2 && C::P_FIRST != 4) {
-        if (need_mask)
-          emit_p_uneven<C::POLY_MOD, false, C::P_FIRST>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
-        else
-          emit_p_uneven<C::POLY_MOD, true, C::P_FIRST>(s, tS, c2, nmc2, lsum2, &p_full[2 * h]);
-      } else {
-        if (need_mask)
-          emit_p<C::POLY_MOD, false, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
-        else
-          emit_p<C::POLY_MOD, true, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
-      }
+      if (need_mask)
+        emit_p<C::POLY_MOD, false, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
+      else
+        emit_p<C::POLY_MOD, true, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
       TR_TRACE_AT(3, j);
     }
     float l;

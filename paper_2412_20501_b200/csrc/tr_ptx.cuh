@@ -73,25 +73,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// Wait with an explicit suspend-time hint (ns) on every try_wait: the warp
-// sleeps in the barrier unit instead of re-polling (diagnostic builds).
-__device__ __forceinline__ void mbar_wait_hinted(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  const uint32_t addr = smem_u32(bar);
-  const uint64_t t0 = globaltimer_ns();
-  for (uint32_t it = 0;; ++it) {
-    uint32_t ok;
-    asm volatile(
-        "{\n.reg .pred P1;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
-        "selp.u32 %0, 1, 0, P1;\n}\n"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity), "r"(ns)
-        : "memory");
-    if (ok) return;
-    if ((it & 255u) == 255u && globaltimer_ns() - t0 > 20000000000ull) __trap();
-  }
-}
-
 // Wait with nanosleep back-off between polls, for a warp that shares its
 // SM sub-partition with softmax warps: a tight try_wait loop steals their
 // issue slots.  `ns` trades observation latency for issue slots.
@@ -354,11 +335,6 @@ __device__ __forceinline__ void tmem_ld32_at(uint32_t taddr, uint32_t (&r)[N]) {
         "=r"(r[OFF + 24]), "=r"(r[OFF + 25]), "=r"(r[OFF + 26]), "=r"(r[OFF + 27]),
         "=r"(r[OFF + 28]), "=r"(r[OFF + 29]), "=r"(r[OFF + 30]), "=r"(r[OFF + 31])
       : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
-               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
