@@ -28,12 +28,6 @@ struct AttnCfg {
   static constexpr int SMEM = SMEM_TILES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
   static constexpr uint32_t IDESC_QK = idesc_bf16(128, BN, false);
   static constexpr uint32_t IDESC_PV = idesc_bf16(128, D, true);
-  static constexpr uint32_t IDESC_QK64 = idesc_bf16(128, 64, false);
-#ifdef TR_QK_SPLIT
-  static constexpr int P_COL = 64;
-#else
-  static constexpr int P_COL = 0;
-#endif
   static constexpr float RESCALE_LOG2 = 8.0f;
 #ifndef TR_POLY_MOD
 #define TR_POLY_MOD 6

@@ -48,7 +48,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   uint64_t* o_done = p_full + 2 * C::NPC;       // [2]
   int64_t* kv_tiles = reinterpret_cast<int64_t*>(o_done + 2);  // [4]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 6);
-  uint64_t* s_loaded = o_done + 7;              // [2] (TR_QK_SPLIT) S_h(j) is in registers
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -66,7 +65,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       mbar_init(&s_full[h], 1);
       for (int kh = 0; kh < C::NPC; ++kh) mbar_init(&p_full[C::NPC * h + kh], 128);
       mbar_init(&o_done[h], 1);
-      mbar_init(&s_loaded[h], 128);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmq); tma_prefetch_desc(&tmk); tma_prefetch_desc(&tmv);
@@ -156,8 +154,8 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         mma_ss_elect(tmem + 256 + h * 128, desc_add(a0, offa), desc_add(b0, (kk * 2048) >> 4),
                      C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
 #else
-        mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + C::P_COL + kk * 8,
-                     desc_add(b0, (kk * 2048) >> 4), C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
+        mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
+                     C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
 #endif
       }
     };
@@ -169,67 +167,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         pv(h, stage, kh, acc || kh > 0);
       }
     };
-#ifdef TR_QK_SPLIT
-    // S_h = Q_h.K^T as two N=64 MMA groups: keys 0-63 -> S_h columns 0-63
-    // (part 0), keys 64-127 -> columns 64-127 (part 1).  P_h lives in columns
-    // 64-127, so part 0 of the NEXT tile is issued as soon as the softmax has
-    // S_h(j) in registers (s_loaded), and only part 1 waits behind P_h(j).V_j.
-    auto qkp = [&](int h, int stage, int part) {
-      const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
-      const uint64_t b0 = dK + static_cast<uint32_t>((stage * C::TILE + part * 8192) >> 4);
-      #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
-        mma_ss_elect(tmem + h * 128 + 64 * part, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK64,
-                     kk > 0);
-      }
-    };
-    int sk = 0;
-    uint32_t rk = 0;
-    mbar_wait(&kv_full[0], 0);
-    tc_fence_after();
-    qkp(0, 0, 0);
-    qkp(0, 0, 1);
-    tc_commit_elect(&s_full[0]);
-    qkp(1, 0, 0);
-    qkp(1, 0, 1);
-    tc_commit_elect(&s_full[1]);
-    tc_commit_elect(&kv_empty[0]);
-    for (int j = 0; j < ntiles; ++j) {
-      const int sv = (sk + 1 == C::NS) ? 0 : sk + 1;
-      const uint32_t rv = (sk + 1 == C::NS) ? rk + 1 : rk;
-      const int sk1 = (sv + 1 == C::NS) ? 0 : sv + 1;
-      const uint32_t rk1 = (sv + 1 == C::NS) ? rv + 1 : rv;
-      const bool more = j + 1 < ntiles;
-      if (more) {
-        mbar_wait(&s_loaded[0], j & 1);
-        mbar_wait(&kv_full[sk1], rk1 & 1);
-        tc_fence_after();
-        qkp(0, sk1, 0);
-      }
-      mbar_wait(&kv_full[sv], rv & 1);
-      tc_fence_after();
-      pv_both(0, sv, j & 1, j > 0);
-      if (j == ntiles - 1) tc_commit_elect(&o_done[0]);
-      if (more) {
-        qkp(0, sk1, 1);
-        tc_commit_elect(&s_full[0]);
-        mbar_wait(&s_loaded[1], j & 1);
-        tc_fence_after();
-        qkp(1, sk1, 0);
-      }
-      pv_both(1, sv, j & 1, j > 0);
-      tc_commit_elect(&kv_empty[sv]);
-      if (j == ntiles - 1) tc_commit_elect(&o_done[1]);
-      if (more) {
-        qkp(1, sk1, 1);
-        tc_commit_elect(&s_full[1]);
-        tc_commit_elect(&kv_empty[sk1]);
-      }
-      sk = sk1;
-      rk = rk1;
-    }
-#else
     int prev_v_stage = 0;
     int sk = 0;
     uint32_t rk = 0;     // ring position / round of K_j (V_j follows it)
@@ -262,7 +199,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     pv_both(1, prev_v_stage, (ntiles - 1) & 1, ntiles - 1 > 0);
     tc_commit_elect(&kv_empty[prev_v_stage]);
     tc_commit_elect(&o_done[1]);
-#endif
    }
   } else {
    setmaxnreg_inc<224>();
@@ -318,10 +254,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       tmem_ld32_at<64>(tS + 64, s);
       tmem_ld32_at<96>(tS + 96, s);
       tc_wait_ld();
-#ifdef TR_QK_SPLIT
-      tc_fence_before();
-      mbar_arrive(&s_loaded[h]);
-#endif
       if (need_mask) {
         int64_t lim = valid;
         if (p.causal) lim = imin64(lim, my_pos - kpos + 1);
@@ -370,9 +302,9 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       // tiles keep every exp2 on MUFU (exact 0 for -inf); full tiles move one
       // pair in POLY_MOD to the FMA pipe.
       if (need_mask)
-        emit_p<C::POLY_MOD, false, C::NPC>(s, tS + C::P_COL, c2, nmc2, lsum2, &p_full[C::NPC * h]);
+        emit_p<C::POLY_MOD, false, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
       else
-        emit_p<C::POLY_MOD, true, C::NPC>(s, tS + C::P_COL, c2, nmc2, lsum2, &p_full[C::NPC * h]);
+        emit_p<C::POLY_MOD, true, C::NPC>(s, tS, c2, nmc2, lsum2, &p_full[C::NPC * h]);
       TR_TRACE_AT(3, j);
     }
     float l;

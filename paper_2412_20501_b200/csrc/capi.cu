@@ -22,6 +22,9 @@ int fail(int code, const std::string& msg) {
 }
 int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return TR_OK;
+  // the failure is reported here: reset the runtime's (non-sticky) last-error
+  // slot so a later launch check does not report it a second time
+  cudaGetLastError();
   return fail(TR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 

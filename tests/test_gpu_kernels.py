@@ -269,3 +269,10 @@ def test_enable_peer_access(K):
     from paper_2412_20501_b200._lib import CudaError, UnsupportedError
     with pytest.raises((CudaError, UnsupportedError)):
         K.enable_peer_access(torch.cuda.device_count() + 3)
+    # the reported failure does not linger in the runtime's last-error slot
+    # (it once surfaced as the next kernel launch's error)
+    for d in (8, 128):      # CUDA-core and tcgen05 kernels
+        x = torch.zeros(64, 1, d, dtype=torch.bfloat16, device="cuda")
+        out, lse = K.attention_block(x, x, x, 0)
+        torch.cuda.synchronize()
+        assert torch.isfinite(lse).all()
