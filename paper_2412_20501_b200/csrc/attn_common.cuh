@@ -53,12 +53,12 @@ struct AttnCfg {
 static __device__ unsigned long long g_trace[2 * 12 * 64 * 8];
 #define TR_TRACE_AT(slot, jj)                                                        \
   do {                                                                               \
-    if (blockIdx.x < 2 && lane == 0 && (jj) < 64)                                    \
+    if (blockIdx.x < 2 && lane == 0 && (jj) >= 0 && (jj) < 64)                                  \
       g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = clock64();      \
   } while (0)
 #define TR_TRACE_GT(slot, jj)                                                        \
   do {                                                                               \
-    if (blockIdx.x < 2 && lane == 0 && (jj) < 64)                                    \
+    if (blockIdx.x < 2 && lane == 0 && (jj) >= 0 && (jj) < 64)                                  \
       g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = globaltimer_ns(); \
   } while (0)
 #else
@@ -126,8 +126,13 @@ __device__ __forceinline__ void cta_tile(const AttnPlan& p, int64_t item, int& h
 // packed accumulators; arrives on pbar[kh] after each of the NPC key chunks.
 template <int POLY_MOD, bool kPoly, int NPC>
 __device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, uint64_t c2,
-                                       uint64_t nmc2, uint64_t (&lsum2)[2], uint64_t* pbar) {
+                                       uint64_t nmc2, uint64_t (&lsum2)[2], uint64_t* pbar,
+                                       int trace_j = -1) {
   constexpr int PAIRS = 64 / NPC;        // bf16 pairs (= TMEM columns) per chunk
+#ifdef TR_TRACE
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#endif
+  (void)trace_j;
   #pragma unroll
   for (int kh = 0; kh < NPC; ++kh) {
     uint32_t pk[PAIRS];
@@ -148,11 +153,13 @@ __device__ __forceinline__ void emit_p(const uint32_t (&s)[128], uint32_t tS, ui
       f2unpack(p2, pa, pb);
       pk[ii] = pack_bf16x2(pa, pb);
     }
+    if (kh < 2) TR_TRACE_AT(4 + 2 * kh, trace_j);     // chunk computed (store issued next)
     if constexpr (PAIRS == 32) tmem_st32(tS + kh * 32, pk);
     else tmem_st16(tS + kh * 16, pk);
     tc_wait_st();
     tc_fence_before();
     mbar_arrive(&pbar[kh]);
+    if (kh < 2) TR_TRACE_AT(5 + 2 * kh, trace_j);     // chunk published
   }
 }
 

@@ -8,7 +8,7 @@ tiles 8..56 of a full 8192x16384 launch, relative to the MMA warp seeing K_j:
   MMA  0 K_j ready   1 S0=Q0.K_j issued   2 P1(j-1) seen, O1 += P1.V(j-1) issued
        3 S1=Q1.K_j issued, V_j ready       4 P0(j) seen, O0 += P0.V_j issued
   softmax warp (half h)  0 wait for S_h(j) starts  1 S_h(j) ready  2 max done
-       3 P_h(j) published
+       3 P_h(j) published; 4/5 first P chunk computed / published, 6/7 second
 """
 import ctypes
 import os
@@ -41,7 +41,11 @@ for w in range(4, 12):
     print(f"softmax warp {w} (half {(w - 4) // 4}, SMSP {w % 4}):",
           [int(np.median(t[w, J, s] - base)) for s in range(4)],
           " S ready->max", int(np.median(t[w, J, 2] - t[w, J, 1])),
-          " max->P", int(np.median(t[w, J, 3] - t[w, J, 2])))
+          " max->P", int(np.median(t[w, J, 3] - t[w, J, 2])),
+          " | chunk0 exp", int(np.median(t[w, J, 4] - t[w, J, 2])),
+          " store+arrive", int(np.median(t[w, J, 5] - t[w, J, 4])),
+          " chunk1 exp", int(np.median(t[w, J, 6] - t[w, J, 5])),
+          " store+arrive", int(np.median(t[w, J, 7] - t[w, J, 6])))
 # per-half: the slowest quarter decides P publication
 for hh in (0, 1):
     last = np.max(t[4 + 4 * hh:8 + 4 * hh, J, 3], axis=0)
