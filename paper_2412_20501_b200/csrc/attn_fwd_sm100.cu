@@ -134,12 +134,6 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     auto qk = [&](int h, int stage) {
       const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
       const uint64_t b0 = dK + static_cast<uint32_t>((stage * C::TILE) >> 4);
-#ifdef TR_MMA_BATCH
-      if constexpr (D == 128) {
-        mma_ss_k128_elect<C::BOX / 16>(tmem + h * 128, a0, b0, C::IDESC_QK, 0u);
-        return;
-      }
-#endif
       #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
@@ -150,13 +144,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     constexpr int KPC = 8 / C::NPC;      // 16-key MMA steps per P chunk
     auto pv = [&](int h, int stage, int kh, bool acc) {
       const uint64_t b0 = dV + static_cast<uint32_t>((stage * C::TILE) >> 4);
-#ifdef TR_MMA_BATCH
-      if constexpr (KPC == 4) {
-        mma_ts_x4_elect(tmem + 256 + h * 128, tmem + h * 128 + kh * 32,
-                        desc_add(b0, (kh * 4 * 2048) >> 4), C::IDESC_PV, acc ? 1u : 0u);
-        return;
-      }
-#endif
+
       #pragma unroll
       for (int k4 = 0; k4 < KPC; ++k4) {
         const int kk = kh * KPC + k4;

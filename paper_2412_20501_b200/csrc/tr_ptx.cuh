@@ -168,47 +168,6 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, u
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-// Batched issue (one elect, descriptor offsets as PTX immediates): the 8
-// K-steps of an SS-mode MMA over K=128 held as two 64-column SW128 boxes of
-// BOX16 16-byte units each (K step kk at ((kk/4)*BOX16 + (kk%4)*2)), the
-// first step overwriting D unless acc.
-template <uint32_t BOX16>
-__device__ __forceinline__ void mma_ss_k128_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                                  uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, t, e;\n.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
-      "setp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
-      "add.s64 a1, %1, 2;\nadd.s64 a2, %1, 4;\nadd.s64 a3, %1, 6;\n"
-      "add.s64 a4, %1, %5;\nadd.s64 a5, a4, 2;\nadd.s64 a6, a4, 4;\nadd.s64 a7, a4, 6;\n"
-      "add.s64 b1, %2, 2;\nadd.s64 b2, %2, 4;\nadd.s64 b3, %2, 6;\n"
-      "add.s64 b4, %2, %5;\nadd.s64 b5, b4, 2;\nadd.s64 b6, b4, 4;\nadd.s64 b7, b4, 6;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, t;\n}\n" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc), "n"(static_cast<uint64_t>(BOX16)));
-}
-// Batched TS-mode issue of 4 consecutive 16-key steps: A (P) from TMEM columns
-// a_tmem + 8k, B (V, MN-major) at b_desc + 128k (2048-byte steps).
-__device__ __forceinline__ void mma_ts_x4_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                                uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p, t, e;\n.reg .b32 a1, a2, a3;\n.reg .b64 b1, b2, b3;\n"
-      "setp.ne.b32 p, %4, 0;\nsetp.eq.b32 t, 0, 0;\n"
-      "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\n"
-      "add.s64 b1, %2, 128;\nadd.s64 b2, %2, 256;\nadd.s64 b3, %2, 384;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc));
-}
 __device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
