@@ -504,7 +504,9 @@ def run_ours(a):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(),
-                         "kernel": "tr::attn_fwd_sm100_kernel<128>",
+                         "kernel": ("tr::attn_fwd_sm100_kernel<128>"
+                                    if os.environ.get("TR_ATTN_PAIR2") == "0"
+                                    else "tr::attn_fwd_pair2_kernel (CTA pairs, cta_group::2)"),
                          "flops_per_launch": attn_flops_per_launch,
                          "avg_launch_ms": attn_avg_ms,
                          "peak_kind": f"bf16_tflops_sustained ({peak_src})",

@@ -16,8 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtokenring.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["capi.cu", "attn_fwd_sm100.cu", "attn_fwd_variants.cu", "attn_simt.cu", "lse_merge.cu",
-           "splitmix.cu", "p2p_flags.cu"]
+SOURCES = ["capi.cu", "attn_fwd_sm100.cu", "attn_fwd_variants.cu", "attn_fwd_pair2.cu", "attn_simt.cu",
+           "lse_merge.cu", "splitmix.cu", "p2p_flags.cu"]
 HEADERS = ["tr_ptx.cuh", "tr_internal.h", "attn_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

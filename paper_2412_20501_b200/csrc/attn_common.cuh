@@ -174,5 +174,7 @@ int launch_attn_variant(const CUtensorMap& tq, const CUtensorMap& tk, const CUte
                         AttnPlan& plan, int head_dim, int64_t blocks, cudaStream_t s);
 int launch_attn_pair(const void* q, const void* k, const void* v, int64_t tq_total,
                      int64_t tk_total, AttnPlan& plan, cudaStream_t s);
+int launch_attn_pair2(const void* q, const void* k, const void* v, int64_t tq_total,
+                      int64_t tk_total, AttnPlan& plan, cudaStream_t s);
 
 }  // namespace tr

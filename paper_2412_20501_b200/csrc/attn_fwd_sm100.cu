@@ -448,11 +448,27 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
 }
 
 
+// D=128: the CTA-pair kernel (attn_fwd_pair2.cu) unless TR_ATTN_PAIR2=0 or one
+// of the diagnostic single-CTA variants (TR_ATTN_PSMEM / TR_ATTN_PERSISTENT)
+// is requested
+static bool use_pair2() {
+  static int v = -1;
+  if (v < 0) {
+    v = 1;
+    if (const char* e = getenv("TR_ATTN_PAIR2")) v = e[0] == '1';
+    for (const char* name : {"TR_ATTN_PSMEM", "TR_ATTN_PERSISTENT"})
+      if (const char* e = getenv(name))
+        if (e[0] == '1') v = 0;
+  }
+  return v == 1;
+}
+
 int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_total,
                       int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s) {
 #ifdef TR_KERNEL_PAIR
   if (head_dim == 128) return launch_attn_pair(q, k, v, tq_total, tk_total, plan, s);
 #else
+  if (head_dim == 128 && use_pair2()) return launch_attn_pair2(q, k, v, tq_total, tk_total, plan, s);
   if (head_dim == 128) return launch_d<128>(q, k, v, tq_total, tk_total, plan, s);
 #endif
   if (head_dim == 64) return launch_d<64>(q, k, v, tq_total, tk_total, plan, s);

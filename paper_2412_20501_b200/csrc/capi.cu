@@ -291,7 +291,7 @@ int tr_enable_peer_access(int32_t peer_device) {
 }
 
 const char* tr_version(void) { return "tokenring-b200 0.1 (sm_100a)"; }
-int32_t tr_kernel_count(void) { return 9; }
+int32_t tr_kernel_count(void) { return 10; }
 const char* tr_last_error(void) { return g_last_error.c_str(); }
 
 }  // extern "C"

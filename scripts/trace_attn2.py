@@ -27,11 +27,17 @@ v = torch.randn(tk, h, d, device="cuda").to(torch.bfloat16)
 for _ in range(3):
     K.attention_block(q, k, v, 0)
 torch.cuda.synchronize()
-buf = np.zeros(12 * 64 * 8, dtype=np.uint64)
+CTA = int(os.environ.get("CTA", "0"))      # 1: the second CTA of a pair build
+buf = np.zeros(2 * 12 * 64 * 8, dtype=np.uint64)
 L = _lib.lib()
-L.tr_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-assert L.tr_debug_trace(buf.ctypes.data, buf.nbytes) == 0
-t = buf.reshape(12, 64, 8).astype(np.int64)
+fn = getattr(L, os.environ.get("TRACE_SYM", "tr_debug_trace"))   # tr_debug_trace_pair2: pair build
+fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+assert fn(buf.ctypes.data, buf.nbytes) == 0
+t_all = buf.reshape(2, 12, 64, 8).astype(np.int64)
+t = t_all[CTA]
+if CTA:   # softmax events of CTA 1 against the leader's MMA warp (cluster-local clocks differ)
+    t = t.copy()
+    t[1] = t_all[0][1]
 J = slice(8, 56)
 base = t[1, J, 0]
 period = np.median(np.diff(t[1, 8:57, 0]))
