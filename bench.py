@@ -465,10 +465,12 @@ def run_ours(a):
     if not a.no_e2e:
         e2e_steps = max(2, a.steps)     # pipeline fill/drain amortised over the K steps
         # head groups: as many as keep each step launch >= ~7 waves of CTAs
-        # (256-row q tiles x heads, one CTA per SM), at most 4
+        # (256-row q tiles x heads, one CTA per SM), at most TR_BENCH_MAX_GROUPS
         ctas_per_head = S // (256 * world)
-        groups = next(g for g in (4, 2, 1)
-                      if H % g == 0 and (g == 1 or ctas_per_head * (H // g) >= 7 * 148))
+        max_g = int(os.environ.get("TR_BENCH_MAX_GROUPS", "4"))
+        groups = next(g for g in (8, 4, 2, 1)
+                      if g <= max_g and H % g == 0
+                      and (g == 1 or ctas_per_head * (H // g) >= 7 * 148))
         def make_runner(hg):
             runners.append(TokenRingAttention(S, hg, D, causal=True, transport=transport))
             return runners[-1]
