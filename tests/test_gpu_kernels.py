@@ -276,3 +276,43 @@ def test_enable_peer_access(K):
         out, lse = K.attention_block(x, x, x, 0)
         torch.cuda.synchronize()
         assert torch.isfinite(lse).all()
+
+
+_SINGLE_CTA_SCRIPT = r"""
+import sys
+import numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import kernels as ok, splitmix
+from paper_2412_20501_b200 import kernels as K
+worst_o = worst_l = 0.0
+for tq, tk, h, mask, qo, ko in [(256, 256, 2, 2, 0, 0), (512, 1024, 3, 0, 0, 0),
+                                (1000, 1000, 2, 2, 0, 0), (129, 257, 1, 2, 128, 0)]:
+    n = max(tq, tk)
+    q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(tq + 5, n, h, 128))
+    q, k, v = q[:tq], k[:tk], v[:tk]
+    ro, rl = ok.attention_block(q, k, v, mask, qo, ko)
+    d = lambda x: torch.as_tensor(np.asarray(x, np.float32)).to(torch.bfloat16).cuda().contiguous()
+    o, l = K.attention_block(d(q), d(k), d(v), mask, qo, ko)
+    torch.cuda.synchronize()
+    o = o.float().cpu().numpy(); l = l.float().cpu().numpy()
+    fin = np.isfinite(rl)
+    assert np.array_equal(np.isfinite(l), fin)
+    worst_l = max(worst_l, float(np.abs(l[fin] - rl[fin]).max()))
+    worst_o = max(worst_o, float(np.abs(o - ro).max()))
+print(worst_o, worst_l)
+"""
+
+
+def test_single_cta_kernel_d128_subprocess():
+    """D=128 runs on the CTA-pair kernel by default; the single-CTA kernel it is
+    built from (TR_ATTN_PAIR2=0, chosen once per process) keeps its parity."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TR_ATTN_PAIR2="0")
+    r = subprocess.run([sys.executable, "-c", _SINGLE_CTA_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    worst_o, worst_l = map(float, r.stdout.split()[-2:])
+    assert worst_o <= OUT_TOL and worst_l <= LSE_TOL, (worst_o, worst_l)
