@@ -268,28 +268,6 @@ __device__ __forceinline__ void tc_commit2_elect(uint64_t* bar) {
       "h"(static_cast<uint16_t>(3))
       : "memory");
 }
-// commit with an explicit destination mask (clusters larger than one pair)
-__device__ __forceinline__ void tc_commit2_mask_elect(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-// TMA load multicast to the CTAs in `mask` (same smem offset in each); the
-// completion bytes are counted on each destination pair's leader barrier
-__device__ __forceinline__ void tma_load_2d_pair_mc_elect(void* smem_dst, const void* tmap,
-                                                          uint32_t leader_bar, int32_t c0, int32_t c1,
-                                                          uint16_t mask, uint64_t cache_hint) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;\n}\n" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask),
-      "l"(cache_hint)
-      : "memory");
-}
 // TMA load into this CTA's shared memory whose completion bytes are counted on
 // the LEADER CTA's barrier (`leader_bar` = shared::cluster address)
 __device__ __forceinline__ void tma_load_2d_pair_elect(void* smem_dst, const void* tmap,
