@@ -295,6 +295,7 @@ for tq, tk, h, mask, qo, ko in [(256, 256, 2, 2, 0, 0), (512, 1024, 3, 0, 0, 0),
     o, l = K.attention_block(d(q), d(k), d(v), mask, qo, ko)
     torch.cuda.synchronize()
     o = o.float().cpu().numpy(); l = l.float().cpu().numpy()
+    np.save({out!r} + f"_{{tq}}_{{tk}}_o.npy", o); np.save({out!r} + f"_{{tq}}_{{tk}}_l.npy", l)
     fin = np.isfinite(rl)
     assert np.array_equal(np.isfinite(l), fin)
     worst_l = max(worst_l, float(np.abs(l[fin] - rl[fin]).max()))
@@ -303,16 +304,26 @@ print(worst_o, worst_l)
 """
 
 
-def test_single_cta_kernel_d128_subprocess():
+def test_single_cta_kernel_d128_subprocess(tmp_path):
     """D=128 runs on the CTA-pair kernel by default; the single-CTA kernel it is
-    built from (TR_ATTN_PAIR2=0, chosen once per process) keeps its parity."""
+    built from (TR_ATTN_PAIR2=0, chosen once per process) keeps its parity, and
+    the two produce bit-identical out and lse (same MMA K order, same softmax)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TR_ATTN_PAIR2="0")
-    r = subprocess.run([sys.executable, "-c", _SINGLE_CTA_SCRIPT.format(root=root)], env=env,
-                       capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr[-2000:]
-    worst_o, worst_l = map(float, r.stdout.split()[-2:])
-    assert worst_o <= OUT_TOL and worst_l <= LSE_TOL, (worst_o, worst_l)
+    runs = {}
+    for flag in ("0", "1"):
+        out = str(tmp_path / f"pair{flag}")
+        env = dict(os.environ, TR_ATTN_PAIR2=flag)
+        r = subprocess.run([sys.executable, "-c", _SINGLE_CTA_SCRIPT.format(root=root, out=out)],
+                           env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        worst_o, worst_l = map(float, r.stdout.split()[-2:])
+        assert worst_o <= OUT_TOL and worst_l <= LSE_TOL, (flag, worst_o, worst_l)
+        runs[flag] = out
+    for tq, tk in [(256, 256), (512, 1024), (1000, 1000), (129, 257)]:
+        for part in ("o", "l"):
+            a = np.load(runs["0"] + f"_{tq}_{tk}_{part}.npy")
+            b = np.load(runs["1"] + f"_{tq}_{tk}_{part}.npy")
+            assert np.array_equal(a, b), (tq, tk, part)
