@@ -18,7 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_vec8 -c 1 \
   -o gpurun_out/merge_${TAG} -f \
   python scripts/probe_merge.py > gpurun_out/merge_ncu_${TAG}.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_n_vec8 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_n_bf16 -c 1 \
   -o gpurun_out/merge_n_${TAG} -f \
   python scripts/probe_merge.py > gpurun_out/merge_n_ncu_${TAG}.log 2>&1
 ls -la gpurun_out
