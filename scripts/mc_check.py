@@ -1,3 +1,10 @@
+"""Kernel-vs-kernel check (diagnostic): run a few D=128 shapes through the
+current library and save out/lse, so two runs with different kernel choices
+(TR_ATTN_PAIR2=0/1, or TOKENRING_LIB=<variant build>) can be compared bitwise.
+
+    TR_ATTN_PAIR2=0 python scripts/mc_check.py /tmp/a.pt
+    TR_ATTN_PAIR2=1 python scripts/mc_check.py /tmp/b.pt
+"""
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2412_20501_b200 import kernels as K
