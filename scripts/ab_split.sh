@@ -1,4 +1,7 @@
 #!/bin/bash
+# HISTORICAL: A/B of the split-row softmax experiment (TR_ATTN_SPLIT), which
+# exists only in commit 44ba687 (check it out to rerun); the result is in
+# profiles/r01/split_softmax_ab.log and DESIGN.md section 5.
 set -u
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
