@@ -307,7 +307,8 @@ print(worst_o, worst_l)
 def test_single_cta_kernel_d128_subprocess(tmp_path):
     """D=128 runs on the CTA-pair kernel by default; the single-CTA kernel it is
     built from (TR_ATTN_PAIR2=0, chosen once per process) keeps its parity, and
-    the two produce bit-identical out and lse (same MMA K order, same softmax)."""
+    the two agree closely (same MMA K order and softmax; they differ only in
+    which exp2 pairs go through the polynomial: 1 in 8 vs 1 in 6)."""
     import os
     import subprocess
     import sys
@@ -326,4 +327,7 @@ def test_single_cta_kernel_d128_subprocess(tmp_path):
         for part in ("o", "l"):
             a = np.load(runs["0"] + f"_{tq}_{tk}_{part}.npy")
             b = np.load(runs["1"] + f"_{tq}_{tk}_{part}.npy")
-            assert np.array_equal(a, b), (tq, tk, part)
+            assert np.array_equal(np.isfinite(a), np.isfinite(b)), (tq, tk, part)
+            fin = np.isfinite(a)
+            tol = 1e-2 if part == "o" else 1e-4      # one bf16 ulp near 1 / fp32 sums
+            assert np.abs(a[fin] - b[fin]).max() <= tol, (tq, tk, part, np.abs(a[fin] - b[fin]).max())
