@@ -49,6 +49,13 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="token-ring", choices=["token-ring", "ring"],
+                    help="token-ring (default: zigzag TokenRing when causal, the metric's "
+                         "workload) or ring (Ring Attention KV rotation, ref engine.py:203-230: "
+                         "the config-4 baseline)")
+    ap.add_argument("--non-causal", action="store_true",
+                    help="non-causal attention (config-4 sweep; TokenRing then uses the "
+                         "contiguous partition)")
     ap.add_argument("--transport", default="fused", choices=["nccl", "ipc", "fused"],
                     help="N>1 exchange: fused (default: Q by copy engines into the peer's "
                          "IPC-mapped buffer, OUT rows stored by the attention epilogue straight "
@@ -61,11 +68,27 @@ def causal_flops(S, H, D):
     return 4 * H * D * (S * (S + 1) // 2)
 
 
+def workload_flops(a):
+    return 4 * a.heads * a.head_dim * a.seq * a.seq if a.non_causal else \
+        causal_flops(a.seq, a.heads, a.head_dim)
+
+
+def schedule_name(a, n):
+    if a.schedule == "ring":
+        name = "ring (Ring Attention, KV rotation)"
+    else:
+        name = "token-ring" if a.non_causal else "zigzag-token-ring"
+    return name if n > 1 else name + " (P=1 trivial)"
+
+
 def workload_config(a, n):
-    return {"workload": f"zigzag TokenRing fwd, S={a.seq}, H={a.heads}, D={a.head_dim}, causal, "
+    mask = "non-causal" if a.non_causal else "causal"
+    label = "Ring Attention" if a.schedule == "ring" else (
+        "TokenRing" if a.non_causal else "zigzag TokenRing")
+    return {"workload": f"{label} fwd, S={a.seq}, H={a.heads}, D={a.head_dim}, {mask}, "
                         f"bf16, {n} rank(s)",
             "seq_len": a.seq, "heads": a.heads, "head_dim": a.head_dim, "ranks": n,
-            "schedule": "zigzag-token-ring" if n > 1 else "zigzag-token-ring (P=1 trivial)",
+            "schedule": schedule_name(a, n), "causal": not a.non_causal,
             "global_batch": 1, "parallelism": f"sp{n}",
             "l2": "inputs larger than L2 (each q/k/v tensor >= 1 GiB at S=131072), no flush"}
 
@@ -390,11 +413,12 @@ def run_ours(a):
             print(f"bench: no P2P path between all GPUs; transport {transport} -> nccl",
                   file=sys.stderr)
             transport = "nccl"
-    runner = TokenRingAttention(S, H, D, causal=True, record_timeline=True,
-                                transport=transport)
+    causal = not a.non_causal
+    runner = TokenRingAttention(S, H, D, causal=causal, record_timeline=True,
+                                transport=transport, schedule=a.schedule)
     runners = [runner]
     q, k, v = rng.local_inputs(a.seed, runner.part, rank, H, D)
-    total_flops = causal_flops(S, H, D)
+    total_flops = workload_flops(a)
 
     def barrier():
         if world > 1:
@@ -472,7 +496,8 @@ def run_ours(a):
                       if g <= max_g and H % g == 0
                       and (g == 1 or ctas_per_head * (H // g) >= 7 * 148))
         def make_runner(hg):
-            runners.append(TokenRingAttention(S, hg, D, causal=True, transport=transport))
+            runners.append(TokenRingAttention(S, hg, D, causal=causal, transport=transport,
+                                              schedule=a.schedule))
             return runners[-1]
         e2e_ms = e2e_pipelined(make_runner, q, k, v, e2e_steps, barrier, allmax, groups)
         h2d = 3 * q.numel() * 2 * world
@@ -506,9 +531,7 @@ def run_ours(a):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(),
-                         "kernel": ("tr::attn_fwd_sm100_kernel<128>"
-                                    if os.environ.get("TR_ATTN_PAIR2") == "0"
-                                    else "tr::attn_fwd_pair2_kernel (CTA pairs, cta_group::2)"),
+                         "kernel": "tr::attn_fwd_pair2_kernel (CTA pairs, cta_group::2)",
                          "flops_per_launch": attn_flops_per_launch,
                          "avg_launch_ms": attn_avg_ms,
                          "peak_kind": f"bf16_tflops_sustained ({peak_src})",

@@ -3,8 +3,10 @@
  * attention path.
  *
  * Every entry point takes plain device pointers, sizes and a cudaStream_t
- * passed as void*; none of them allocates, synchronises the device or keeps
- * state across calls (except tr_p2p_* which own a per-process peer table).
+ * passed as void*; none of them synchronises the device.  The only state kept
+ * across calls is per process: the kernels' shared-memory attribute (set once
+ * per device), the pinned status block of the flag waits (tr_poll_error) and
+ * the calling thread's last error message.
  * All return TR_OK (0) or a negative status; the message of the last failure
  * on the calling thread is available from tr_last_error().
  *
@@ -39,6 +41,7 @@ extern "C" {
 #define TR_ERR_CONFIG -3      /* ConfigError */
 #define TR_ERR_CUDA -4        /* CUDA runtime / driver failure */
 #define TR_ERR_UNSUPPORTED -5 /* shape the sm_100a kernels do not cover */
+#define TR_ERR_TIMEOUT -6     /* ScheduleError: a message never arrived (tr_poll_error) */
 
 /* mask kinds, identical to ringsim.kernels.MASK_* (pkg/src/ringsim/kernels.py:33-35) */
 #define TR_MASK_NONE 0
@@ -146,9 +149,24 @@ int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
  * TR_ERR_UNSUPPORTED if the two devices have no P2P path. */
 int tr_enable_peer_access(int32_t peer_device);
 
-/* Version / capability probes (no GPU work). */
+/* A tr_flag_wait that times out (a lost or never-sent message; default 30 s)
+ * does not trap -- that would kill the CUDA context -- but records the flag,
+ * the expected and the observed value in a pinned host-mapped block and lets
+ * the stream go on (its results are then invalid).  tr_poll_error() reads that
+ * block without touching the device: TR_OK, or TR_ERR_TIMEOUT with the record
+ * in tr_last_error() (the reference raises ScheduleError for an undelivered
+ * message, engine.py:532-537).  tr_clear_error() re-arms it;
+ * tr_set_flag_timeout_ms() changes the timeout of later waits (tests). */
+int tr_poll_error(void);
+void tr_clear_error(void);
+void tr_set_flag_timeout_ms(uint64_t ms);
+
+/* Version / capability probes (no GPU work).  tr_kernel_count() is the number
+ * of __global__ kernels (templates counted once) in the library and
+ * tr_kernel_name(i) their names, i in [0, count) (NULL outside). */
 const char* tr_version(void);
 int32_t tr_kernel_count(void);
+const char* tr_kernel_name(int32_t i);
 const char* tr_last_error(void);
 
 #ifdef __cplusplus

@@ -3,17 +3,19 @@
 The library is built in-tree (``python -m paper_2412_20501_b200.build``).  There
 is no fallback: if the shared object is missing or fails to load, every
 compute entry point raises -- the product path never silently degrades to a
-CPU or PyTorch implementation.
+CPU or PyTorch implementation.  There is no library-selection switch either:
+the product loads ``libtokenring.so`` next to this file (A/B scripts and the
+experiments build load their own libraries explicitly, see ``load_library``).
 """
 
 import ctypes
 import os
 import threading
 
-from .errors import ConfigError, DimensionError, InputError, RingsimError
+from .errors import ConfigError, DimensionError, InputError, RingsimError, ScheduleError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("TOKENRING_LIB") or os.path.join(HERE, "libtokenring.so")
+LIB_PATH = os.path.join(HERE, "libtokenring.so")
 
 TR_OK = 0
 TR_ERR_DIMENSION = -1
@@ -21,6 +23,7 @@ TR_ERR_INPUT = -2
 TR_ERR_CONFIG = -3
 TR_ERR_CUDA = -4
 TR_ERR_UNSUPPORTED = -5
+TR_ERR_TIMEOUT = -6
 
 TR_DTYPE_F32 = 0
 TR_DTYPE_BF16 = 1
@@ -30,8 +33,9 @@ TR_MERGE_MAX = 16
 EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
            "tr_merge_state", "tr_merge_n", "tr_partial_init",
            "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_copy_async",
-           "tr_enable_peer_access", "tr_version",
-           "tr_kernel_count", "tr_last_error")
+           "tr_enable_peer_access", "tr_poll_error", "tr_clear_error",
+           "tr_set_flag_timeout_ms", "tr_version",
+           "tr_kernel_count", "tr_kernel_name", "tr_last_error")
 
 
 class CudaError(RingsimError, RuntimeError):
@@ -71,32 +75,53 @@ def _declare(lib):
     lib.tr_flag_wait.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tr_copy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
     lib.tr_enable_peer_access.argtypes = [i32]
+    lib.tr_poll_error.argtypes = []
+    lib.tr_clear_error.argtypes = []
+    lib.tr_clear_error.restype = None
+    lib.tr_set_flag_timeout_ms.argtypes = [ctypes.c_uint64]
+    lib.tr_set_flag_timeout_ms.restype = None
     for name in ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
                  "tr_merge_state", "tr_merge_n",
                  "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
-                 "tr_copy_async", "tr_enable_peer_access"):
+                 "tr_copy_async", "tr_enable_peer_access", "tr_poll_error"):
         getattr(lib, name).restype = ctypes.c_int
     lib.tr_version.restype = ctypes.c_char_p
     lib.tr_version.argtypes = []
     lib.tr_kernel_count.restype = ctypes.c_int32
     lib.tr_kernel_count.argtypes = []
+    lib.tr_kernel_name.restype = ctypes.c_char_p
+    lib.tr_kernel_name.argtypes = [i32]
     lib.tr_last_error.restype = ctypes.c_char_p
     lib.tr_last_error.argtypes = []
 
 
+def load_library(path):
+    """ctypes handle of a libtokenring build at ``path`` with the C ABI declared."""
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built; run `python -m paper_2412_20501_b200.build` "
+                          "(there is no CPU fallback)")
+    handle = ctypes.CDLL(path)
+    _declare(handle)
+    return handle
+
+
 def lib():
-    """Load (once) and return the ctypes handle; raises if it is not built."""
+    """Load (once) and return the product library; raises if it is not built."""
     global _lib
     if _lib is None:
         with _lock:
             if _lib is None:
-                if not os.path.exists(LIB_PATH):
-                    raise ImportError(
-                        f"{LIB_PATH} is not built; run `python -m paper_2412_20501_b200.build` "
-                        "(there is no CPU fallback)")
-                handle = ctypes.CDLL(LIB_PATH)
-                _declare(handle)
-                _lib = handle
+                _lib = load_library(LIB_PATH)
+    return _lib
+
+
+def use_library(path):
+    """Point this process at another build of the library (A/B scripts and the
+    experiments build only -- never the product path).  Call before any
+    compute call."""
+    global _lib
+    with _lock:
+        _lib = load_library(path)
     return _lib
 
 
@@ -113,4 +138,6 @@ def check(status):
         raise ConfigError(msg)
     if status == TR_ERR_UNSUPPORTED:
         raise UnsupportedError(msg)
+    if status == TR_ERR_TIMEOUT:
+        raise ScheduleError(msg)
     raise CudaError(msg)

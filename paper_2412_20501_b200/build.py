@@ -3,6 +3,10 @@ built library travels to the GPU box with the repository snapshot).
 
     python -m paper_2412_20501_b200.build          # incremental
     python -m paper_2412_20501_b200.build --force
+    python -m paper_2412_20501_b200.build --experiments
+        # A/B build (not the product): + the measured-and-rejected kernel
+        # variants of attn_fwd_variants.cu and their TR_ATTN_* run-time
+        # switches, -> _variants/libtokenring_exp.so
 """
 
 import argparse
@@ -16,8 +20,10 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtokenring.so")
 ROOT = os.path.dirname(HERE)
 
-SOURCES = ["capi.cu", "attn_fwd_sm100.cu", "attn_fwd_variants.cu", "attn_fwd_pair2.cu", "attn_simt.cu",
+SOURCES = ["capi.cu", "attn_fwd_sm100.cu", "attn_fwd_pair2.cu", "attn_simt.cu",
            "lse_merge.cu", "splitmix.cu", "p2p_flags.cu"]
+EXPERIMENT_SOURCES = ["attn_fwd_variants.cu"]
+EXP_LIB = os.path.join(HERE, "_variants", "libtokenring_exp.so")
 HEADERS = ["tr_ptx.cuh", "tr_internal.h", "attn_common.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -34,13 +40,19 @@ def _stale():
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.abspath(__file__))
     deps.append(os.path.join(ROOT, "include", "tokenring.h"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, defines=(), out=None):
+def build(force=False, verbose=False, defines=(), out=None, experiments=False):
     """Compile every .cu and link libtokenring.so (or ``out`` -- tuning
-    variants built with extra -D ``defines``)."""
+    variants built with extra -D ``defines``).  ``experiments`` adds the
+    rejected kernel variants and their run-time switches (never the product)."""
+    if experiments:
+        defines = tuple(defines) + ("TR_EXPERIMENTS",)
+        out = out or EXP_LIB
+        os.makedirs(os.path.dirname(out), exist_ok=True)
     lib = out or LIB
     if not force and not defines and not _stale():
         return LIB
@@ -54,7 +66,7 @@ def build(force=False, verbose=False, defines=(), out=None):
     if verbose:
         common += ["-Xptxas", "-v"]
     procs = []
-    for src in SOURCES:
+    for src in SOURCES + (EXPERIMENT_SOURCES if experiments else []):
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
         objs.append(obj)
         procs.append((src, subprocess.Popen(common + ["-c", os.path.join(CSRC, src), "-o", obj],
@@ -79,8 +91,10 @@ def main(argv=None):
     ap.add_argument("-v", "--verbose", action="store_true")
     ap.add_argument("-D", dest="defines", action="append", default=[])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--experiments", action="store_true")
     a = ap.parse_args(argv)
-    print(build(force=a.force, verbose=a.verbose, defines=tuple(a.defines), out=a.out))
+    print(build(force=a.force, verbose=a.verbose, defines=tuple(a.defines), out=a.out,
+                experiments=a.experiments))
 
 
 if __name__ == "__main__":

@@ -430,27 +430,28 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
   if ((rc = make_tmap(&tq, q, tq_total, row_elems))) return rc;
   if ((rc = make_tmap(&tk, k, tk_total, row_elems))) return rc;
   if ((rc = make_tmap(&tv, v, tk_total, row_elems))) return rc;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn_fwd_sm100)");
-    attr_done = true;
-  }
+  int rc2;
+  if ((rc2 = set_smem_attr_once(reinterpret_cast<const void*>(attn_fwd_sm100_kernel<D>), C::SMEM,
+                                "cudaFuncSetAttribute(attn_fwd_sm100)")))
+    return rc2;
   const int64_t blocks = plan.tile_prefix[plan.nq] * plan.heads;
   if (blocks == 0) return TR_OK;
   if (blocks > 0x7FFFFFFF) return fail(TR_ERR_UNSUPPORTED, "grid too large");
-  // opt-in measured alternatives (TR_ATTN_PSMEM / TR_ATTN_PERSISTENT)
+#ifdef TR_EXPERIMENTS
+  // experiments build only: measured-and-rejected alternatives (TR_ATTN_PSMEM /
+  // TR_ATTN_PERSISTENT, attn_fwd_variants.cu); the product library has no
+  // run-time kernel switch
   const int vrc = launch_attn_variant(tq, tk, tv, plan, D, blocks, s);
   if (vrc != -1) return vrc;
+#endif
   attn_fwd_sm100_kernel<D><<<static_cast<unsigned>(blocks), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
   return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
 }
 
 
-// D=128: the CTA-pair kernel (attn_fwd_pair2.cu) unless TR_ATTN_PAIR2=0 or one
-// of the diagnostic single-CTA variants (TR_ATTN_PSMEM / TR_ATTN_PERSISTENT)
-// is requested
+#ifdef TR_EXPERIMENTS
+// experiments build: D=128 on the single-CTA kernel with TR_ATTN_PAIR2=0 or one
+// of the single-CTA variants (A/B and the pair-vs-single parity test only)
 static bool use_pair2() {
   static int v = -1;
   if (v < 0) {
@@ -462,6 +463,9 @@ static bool use_pair2() {
   }
   return v == 1;
 }
+#else
+static constexpr bool use_pair2() { return true; }
+#endif
 
 int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_total,
                       int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s) {

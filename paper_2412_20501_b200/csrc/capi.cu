@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -26,6 +28,21 @@ int cuda_status(cudaError_t e, const char* what) {
   // slot so a later launch check does not report it a second time
   cudaGetLastError();
   return fail(TR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int set_smem_attr_once(const void* func, int bytes, const char* what) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({func, dev})) return TR_OK;
+  if ((rc = cuda_status(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        what)))
+    return rc;
+  done.insert({func, dev});
+  return TR_OK;
 }
 
 int launch_merge(float* acc_out, float* acc_lse, const void* blk_out, int blk_dtype,
@@ -145,7 +162,13 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   for (int i = 0; i < plan.nq; ++i)
     plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
   order_ctas(plan, head_dim);
-  if (sm100_supports(head_dim, heads, q, k, v, out) && plan.nkv > 0) {
+  const bool tc = head_dim == 64 || head_dim == 128;   // the tcgen05 kernels' head dims
+  if (tc && !sm100_supports(head_dim, heads, q, k, v, out))
+    return fail(TR_ERR_UNSUPPORTED,
+                "head_dim " + std::to_string(head_dim) + " runs on the tcgen05 kernels, which need "
+                "16-byte aligned q/k/v/out base pointers (TMA); got a misaligned tensor "
+                "(e.g. a view starting at an odd element) -- pass a contiguous copy");
+  if (tc && plan.nkv > 0) {
     // the kernel raises done_flag itself (last CTA); an empty grid does not run
     if ((rc = launch_attn_sm100(q, k, v, tq_total, tk_total, head_dim, plan, s))) return rc;
     return plan.tile_prefix[plan.nq] * heads == 0 ? flag_only() : TR_OK;
@@ -290,8 +313,24 @@ int tr_enable_peer_access(int32_t peer_device) {
   return cuda_status(e, "cudaDeviceEnablePeerAccess");
 }
 
-const char* tr_version(void) { return "tokenring-b200 0.1 (sm_100a)"; }
-int32_t tr_kernel_count(void) { return 10; }
+int tr_poll_error(void) { return poll_flag_error(); }
+void tr_clear_error(void) { clear_flag_error(); }
+void tr_set_flag_timeout_ms(uint64_t ms) { set_flag_timeout_ns(ms * 1000000ull); }
+
+// every __global__ kernel of the product library (templates once);
+// tests/test_abi.py checks this list against the cubin's symbol table
+static const char* const kKernels[] = {
+    "attn_fwd_pair2_kernel",  "attn_fwd_sm100_kernel", "attn_simt_kernel",
+    "merge_vec8_kernel",      "merge_scalar_kernel",   "merge_scalar_lse_kernel",
+    "merge_n_vec8_kernel",    "merge_n_bf16_kernel",   "merge_n_scalar_kernel",
+    "merge_n_lse_kernel",     "fill_kernel",
+    "flag_set_kernel",        "flag_wait_kernel",      "splitmix_bf16_kernel"};
+
+const char* tr_version(void) { return "tokenring-b200 0.2 (sm_100a)"; }
+int32_t tr_kernel_count(void) { return int32_t(sizeof(kKernels) / sizeof(kKernels[0])); }
+const char* tr_kernel_name(int32_t i) {
+  return i >= 0 && i < tr_kernel_count() ? kKernels[i] : nullptr;
+}
 const char* tr_last_error(void) { return g_last_error.c_str(); }
 
 }  // extern "C"

@@ -14,6 +14,9 @@ constexpr int TR_ORDER_MAX = 2048;   // (segment, tile) classes an explicit CTA 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_status(cudaError_t e, const char* what);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, so a process driving several GPUs sets it on each
+int set_smem_attr_once(const void* func, int bytes, const char* what);
 
 struct AttnPlan {
   tr_segment q[TR_MAX_SEGMENTS];
@@ -63,6 +66,10 @@ int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_to
                       int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s);
 // generic CUDA-core kernel for any head_dim <= 256 (small shapes, odd dims)
 int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s);
+// host-mapped record of a timed-out flag wait (p2p_flags.cu)
+int poll_flag_error();
+void clear_flag_error();
+void set_flag_timeout_ns(unsigned long long ns);
 int launch_attn_simt(const void* q, const void* k, const void* v, int head_dim, AttnPlan& plan,
                      cudaStream_t s);
 bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const void* v,

@@ -44,6 +44,13 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _on(t):
+    """Make ``t``'s device current for a C-ABI call: the library launches on
+    the calling thread's current device (and sets per-device kernel
+    attributes there), so a process driving several GPUs must switch."""
+    return torch.cuda.device(t.device)
+
+
 def _require_cuda(name, t, dtype=None):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise DimensionError(f"{name} must be a CUDA tensor")
@@ -76,9 +83,16 @@ def attention_block(q, k, v, mask_kind=MASK_NONE, q_offset=0, k_offset=0, out=No
         lse = torch.empty((h, tq), dtype=torch.float32, device=q.device)
     _require_cuda("out", out, torch.bfloat16)
     _require_cuda("lse", lse, torch.float32)
-    _lib.check(_lib.lib().tr_attention_block(
-        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), tq, tk, h, d, int(mask_kind),
-        int(q_offset), int(k_offset), _stream(q.device)))
+    if tuple(out.shape) != (tq, h, d) or tuple(lse.shape) != (h, tq):
+        raise DimensionError(f"out must be {(tq, h, d)} and lse {(h, tq)}, got "
+                             f"{tuple(out.shape)} / {tuple(lse.shape)}")
+    for n, t in (("k", k), ("v", v), ("out", out), ("lse", lse)):
+        if t.device != q.device:
+            raise DimensionError(f"{n} is on {t.device}, q on {q.device}")
+    with _on(q):
+        _lib.check(_lib.lib().tr_attention_block(
+            _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), tq, tk, h, d, int(mask_kind),
+            int(q_offset), int(k_offset), _stream(q.device)))
     _count(1)
     return out, lse
 
@@ -104,10 +118,11 @@ def attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse):
         raise DimensionError("out/lse must match q's (T,H,D) / (H,T)")
     qs, ks = _segs(q_segs), _segs(kv_segs)
     dt = _lib.TR_DTYPE_F32 if out.dtype == torch.float32 else _lib.TR_DTYPE_BF16
-    _lib.check(_lib.lib().tr_attention_segments(
-        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
-        q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, dt,
-        _stream(q.device)))
+    with _on(q):
+        _lib.check(_lib.lib().tr_attention_segments(
+            _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
+            q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, dt,
+            _stream(q.device)))
     _count(1)
     return out, lse
 
@@ -138,11 +153,12 @@ def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shif
         _require_cuda("done_flag", done_flag, torch.int64)
         _require_cuda("done_count", done_count, torch.int32)
     qs, ks = _segs(q_segs), _segs(kv_segs)
-    _lib.check(_lib.lib().tr_attention_segments_push(
-        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
-        q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, row_shift, n,
-        None if done_count is None else _ptr(done_count),
-        None if done_flag is None else _ptr(done_flag), done_value, _stream(q.device)))
+    with _on(q):
+        _lib.check(_lib.lib().tr_attention_segments_push(
+            _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
+            q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, row_shift, n,
+            None if done_count is None else _ptr(done_count),
+            None if done_flag is None else _ptr(done_flag), done_value, _stream(q.device)))
     _count(1)
     return out, lse
 
@@ -167,9 +183,10 @@ def merge_state_(acc_out, acc_lse, blk_out, blk_lse, final_out=None):
     if final_out is not None:
         _require_cuda("final_out", final_out, torch.bfloat16)
         fin = _ptr(final_out)
-    _lib.check(_lib.lib().tr_merge_state(
-        _ptr(acc_out), _ptr(acc_lse), _ptr(blk_out), dt, _ptr(blk_lse), t, h, d,
-        acc_lse.stride(0), blk_lse.stride(0), fin, _stream(acc_out.device)))
+    with _on(acc_out):
+        _lib.check(_lib.lib().tr_merge_state(
+            _ptr(acc_out), _ptr(acc_lse), _ptr(blk_out), dt, _ptr(blk_lse), t, h, d,
+            acc_lse.stride(0), blk_lse.stride(0), fin, _stream(acc_out.device)))
     _count(2)
     return acc_out, acc_lse
 
@@ -202,9 +219,10 @@ def merge_n_(acc_out, acc_lse, blocks, final_out=None):
         lses = (ctypes.c_void_p * max(1, n))(*[bl.data_ptr() for _, bl in grp])
         strides = (ctypes.c_int64 * max(1, n))(*[bl.stride(0) for _, bl in grp])
         fin = _ptr(final_out) if final_out is not None and gi == len(groups or [[]]) - 1 else None
-        _lib.check(_lib.lib().tr_merge_n(
-            _ptr(acc_out), _ptr(acc_lse), acc_lse.stride(0), outs, dt, lses, strides, n, t, h, d,
-            fin, _stream(acc_out.device)))
+        with _on(acc_out):
+            _lib.check(_lib.lib().tr_merge_n(
+                _ptr(acc_out), _ptr(acc_lse), acc_lse.stride(0), outs, dt, lses, strides, n, t, h,
+                d, fin, _stream(acc_out.device)))
         _count(2)
     return acc_out, acc_lse
 
@@ -219,8 +237,11 @@ def partial_init_(acc_out, acc_lse):
     _require_cuda("acc_out", acc_out, torch.float32)
     _require_cuda("acc_lse", acc_lse, torch.float32)
     t, h, d = acc_out.shape
-    _lib.check(_lib.lib().tr_partial_init(_ptr(acc_out), _ptr(acc_lse), t, h, d,
-                                          _stream(acc_out.device)))
+    if tuple(acc_lse.shape) != (h, t):
+        raise DimensionError(f"acc_lse must be {(h, t)}, got {tuple(acc_lse.shape)}")
+    with _on(acc_out):
+        _lib.check(_lib.lib().tr_partial_init(_ptr(acc_out), _ptr(acc_lse), t, h, d,
+                                              _stream(acc_out.device)))
     _count(1)
     return acc_out, acc_lse
 
@@ -228,9 +249,10 @@ def partial_init_(acc_out, acc_lse):
 def splitmix_bf16_(dst, seed, first, low=-1.0, high=1.0):
     """Fill contiguous bf16 ``dst`` with SplitMix64 draws first.. of ``seed``."""
     _require_cuda("dst", dst, torch.bfloat16)
-    _lib.check(_lib.lib().tr_splitmix_bf16(
-        ctypes.c_uint64(int(seed) % (1 << 64)), int(first), dst.numel(), float(low), float(high),
-        _ptr(dst), _stream(dst.device)))
+    with _on(dst):
+        _lib.check(_lib.lib().tr_splitmix_bf16(
+            ctypes.c_uint64(int(seed) % (1 << 64)), int(first), dst.numel(), float(low),
+            float(high), _ptr(dst), _stream(dst.device)))
     _count(1)
     return dst
 
@@ -239,14 +261,16 @@ def flag_set_(flag, value, stream=None):
     """Raise a (possibly peer-mapped) int64 sequence flag after all prior work
     on ``stream`` (system-scope release store)."""
     s = stream or torch.cuda.current_stream(flag.device)
-    _lib.check(_lib.lib().tr_flag_set(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
+    with torch.cuda.device(s.device):
+        _lib.check(_lib.lib().tr_flag_set(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
     _count(1)
 
 
 def flag_wait_(flag, value, stream=None):
     """Make ``stream`` wait until ``flag >= value`` (one-thread acquire spin)."""
     s = stream or torch.cuda.current_stream(flag.device)
-    _lib.check(_lib.lib().tr_flag_wait(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
+    with torch.cuda.device(s.device):
+        _lib.check(_lib.lib().tr_flag_wait(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
     _count(1)
 
 
@@ -258,11 +282,28 @@ def copy_(dst, src, stream=None):
     if not (dst.is_contiguous() and src.is_contiguous()):
         raise DimensionError("copy_ needs contiguous tensors")
     s = stream or torch.cuda.current_stream(src.device)
-    _lib.check(_lib.lib().tr_copy_async(_ptr(dst), _ptr(src), dst.numel() * dst.element_size(),
-                                        ctypes.c_void_p(s.cuda_stream)))
+    with torch.cuda.device(s.device):
+        _lib.check(_lib.lib().tr_copy_async(_ptr(dst), _ptr(src), dst.numel() * dst.element_size(),
+                                            ctypes.c_void_p(s.cuda_stream)))
 
 
 def enable_peer_access(peer_device):
     """Let kernels on the current device dereference ``peer_device`` memory
     (IPC-mapped flags / receive slots of the ipc and fused transports)."""
     _lib.check(_lib.lib().tr_enable_peer_access(int(peer_device)))
+
+
+def poll_error():
+    """Raise ScheduleError if a flag wait of this process has timed out (a
+    message that never arrived; the library records it instead of trapping).
+    Reads pinned host memory only -- no device synchronisation."""
+    _lib.check(_lib.lib().tr_poll_error())
+
+
+def clear_error():
+    _lib.lib().tr_clear_error()
+
+
+def set_flag_timeout_ms(ms):
+    """Timeout of later flag waits (default 30 s); for tests of the failure path."""
+    _lib.lib().tr_set_flag_timeout_ms(int(ms))

@@ -29,9 +29,9 @@ import torch
 import torch.distributed as dist
 
 from . import kernels
-from .core import Partial
-from .engine import (MsgKind, build_hybrid, build_token_ring, build_zigzag_token_ring,
-                     group_computes)
+from .core import MaskKind, Partial
+from .engine import (MsgKind, build_hybrid, build_ring_attention, build_token_ring,
+                     build_zigzag_token_ring, group_computes)
 from .errors import ConfigError, DimensionError, ScheduleError
 
 
@@ -40,6 +40,10 @@ from .errors import ConfigError, DimensionError, ScheduleError
 # fused: ipc for Q; the OUT_LSE messages are written by the attention kernel's
 #        epilogue straight into the home rank's receive slot (NVLink stores)
 TRANSPORTS = ("nccl", "ipc", "fused")
+# token-ring: TokenRing (zigzag when causal, contiguous otherwise; hybrid with
+#             nodes > 1) -- Q forward, OUT_LSE reverse
+# ring:       Ring Attention, KV forward only (the reference's baseline)
+SCHEDULES = ("token-ring", "ring")
 
 
 class CudaOps:
@@ -83,6 +87,7 @@ class RankStep:
     kv_store: int = -1       # -1: the local shard; k >= 0: the k-th received KV block
     send_kv: tuple | None = None   # (dst, ids) of the store, sent after this step
     recv_kv: tuple | None = None   # (src, ids) received during this step
+    q_slot: int = -1         # traveling-Q buffer holding q_layout (-1: the local shard)
 
 
 def compile_rank(sched, rank: int) -> list:
@@ -91,7 +96,7 @@ def compile_rank(sched, rank: int) -> list:
     plans = sched.all_plans()
     home = tuple(c.id for c in sorted((c for c in sched.chunks if c.home == rank),
                                       key=lambda c: c.start))
-    layout = home
+    layout, q_slot = home, -1
     kv_layout, kv_store, n_kv_recv = home, -1, 0
     start = {c.id: c.start for c in sched.chunks}
     prog = []
@@ -100,6 +105,10 @@ def compile_rank(sched, rank: int) -> list:
         if g is None:
             raise ScheduleError(f"step {i} rank {rank}: compute set not expressible as one launch")
         q_ids, kv_ids, acc = g
+        if all(cp.mask.kind is MaskKind.FULLY_MASKED for cp in plan.computes[rank]):
+            # the causal ring's blocks above the diagonal (ref engine.py:216-223):
+            # identity partials, nothing to launch or merge
+            q_ids, kv_ids, acc = (), (), None
         send_q, recv_q, send_out, send_kv, recv_kv = [], [], None, None, None
         for m in plan.sends[rank]:
             if m.kind is MsgKind.Q_BLOCK:
@@ -137,9 +146,11 @@ def compile_rank(sched, rank: int) -> list:
             if b not in kv_layout:
                 raise ScheduleError(f"step {i} rank {rank}: kv chunk {b} not resident")
         prog.append(RankStep(i, layout, q_ids, kv_ids, acc, send_q, recv_q, send_out, recv_out,
-                             kv_layout, kv_store, send_kv, recv_kv))
+                             kv_layout, kv_store, send_kv, recv_kv, q_slot))
         if recv_q:
+            # Q received at step i lands in traveling buffer (i+1) % 2
             layout = tuple(sorted((a for _, ids in recv_q for a in ids), key=start.get))
+            q_slot = (i + 1) % 2
         if recv_kv is not None:
             if send_kv is None:
                 raise ScheduleError(f"step {i} rank {rank}: kv received without handing one on")
@@ -212,13 +223,24 @@ class TokenRingAttention:
     """
 
     def __init__(self, seq_len, heads, head_dim, causal=True, group=None, ops=None,
-                 device=None, record_timeline=False, transport="nccl", route="ring", nodes=1):
+                 device=None, record_timeline=False, transport="nccl", route="ring", nodes=1,
+                 schedule="token-ring"):
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if schedule not in SCHEDULES:
+            raise ConfigError(f"schedule must be one of {SCHEDULES}, got {schedule!r}")
         if route != "ring" and not causal:
             raise ConfigError("route='direct' applies to the causal zigzag schedule only")
-        if nodes > 1:
+        if schedule == "ring":
+            # Ring Attention, the config-4 baseline (ref engine.py:203-230):
+            # contiguous shards, every rank keeps its Q and accumulates locally,
+            # KV blocks rotate to rank+1 -- carried by the same KV-store
+            # machinery as the hybrid schedule's node hand-offs
+            if route != "ring" or nodes > 1:
+                raise ConfigError("schedule='ring' takes no route or nodes")
+            self.sched = build_ring_attention(self.P, seq_len, heads, head_dim, causal)
+        elif nodes > 1:
             # the reference's multi-node schedule (ref engine.py:298-303): TokenRing
             # inside each group of P/nodes ranks, KV rotated across the groups
             if causal:
@@ -380,6 +402,7 @@ class TokenRingAttention:
         its consumers' mappings)."""
         torch.cuda.synchronize(self.device)
         self.peer = {}
+        kernels.poll_error()
 
     def progs(self, r):
         """Rank r's step program (compiled on demand; peers' slot indices)."""
@@ -464,7 +487,7 @@ class TokenRingAttention:
                 self._merge_returned((ids, self.out_recv[:n],
                                       self.lse_recv.view(-1)[: H * n].view(H, n)), local_layout)
                 kernels.flag_set_(self.flags[3:4], base + i - 1, cur)
-            cur_q = self.qbuf[i % 2] if i > 0 else q_loc
+            cur_q = self.qbuf[st.q_slot] if st.q_slot >= 0 else q_loc
             kst, vst, kv_lay, kv_local = self._kv_store(st, k_loc, v_loc)
             ev_q = torch.cuda.Event()
             ev_q.record(cur)
@@ -606,7 +629,19 @@ class TokenRingAttention:
                 self.ops.merge_n_(self.acc_out[l0:l0 + c], self.acc_lse[:, l0:l0 + c], blocks)
 
     def __call__(self, q_loc, k_loc, v_loc) -> Partial:
+        """One forward over this rank's shard; returns this rank's home rows.
+
+        The returned Partial's tensors are the runner's own float32
+        accumulator (no copy is made): they hold this call's result only
+        until the next call on the same runner, which overwrites them
+        asynchronously on the device.  Clone them (or copy them out, as
+        bench.py's e2e path does) before calling again.
+
+        ipc / fused transports: a message that never arrives makes the
+        device-side wait time out (30 s) instead of hanging or trapping;
+        the next call (or ``close``) raises ScheduleError for it."""
         if self.transport in ("ipc", "fused"):
+            kernels.poll_error()
             shape = (self.local_rows, self.H, self.D)
             for n, t in (("q", q_loc), ("k", k_loc), ("v", v_loc)):
                 if tuple(t.shape) != shape:
@@ -639,7 +674,7 @@ class TokenRingAttention:
             if pending_out:
                 self._merge_returned(pending_out, local_layout)
             sends, recvs = [], []
-            cur = self.qbuf[i % 2] if i > 0 else q_loc
+            cur = self.qbuf[st.q_slot] if st.q_slot >= 0 else q_loc
             kst, vst, kv_lay, kv_local = self._kv_store(st, k_loc, v_loc)
             for dst, ids, from_home in st.send_q:
                 src_buf, src_layout = (q_loc, local_layout) if from_home else (cur, st.q_layout)

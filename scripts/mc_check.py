@@ -7,6 +7,9 @@ current library and save out/lse, so two runs with different kernel choices
 """
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _ablib import maybe_use_env_library  # noqa: E402
+maybe_use_env_library()
 from paper_2412_20501_b200 import kernels as K
 torch.manual_seed(0)
 res = {}

@@ -13,6 +13,9 @@ import time
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _ablib import maybe_use_env_library  # noqa: E402
+maybe_use_env_library()
 
 
 def sampler(stop, rows):

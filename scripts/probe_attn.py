@@ -9,6 +9,9 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _ablib import maybe_use_env_library  # noqa: E402
+maybe_use_env_library()
 from paper_2412_20501_b200 import kernels as K  # noqa: E402
 
 

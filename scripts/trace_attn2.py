@@ -18,6 +18,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from _ablib import maybe_use_env_library  # noqa: E402
+maybe_use_env_library()
 from paper_2412_20501_b200 import _lib, kernels as K  # noqa: E402
 
 tq, tk, h, d = 8192, 16384, 32, 128

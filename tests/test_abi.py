@@ -33,8 +33,9 @@ def test_header_declares_expected_api():
     assert fns == sorted(["tr_attention_block", "tr_attention_segments",
                           "tr_attention_segments_push", "tr_merge_state", "tr_merge_n",
                           "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
-                          "tr_copy_async", "tr_enable_peer_access", "tr_version",
-                          "tr_kernel_count", "tr_last_error"])
+                          "tr_copy_async", "tr_enable_peer_access", "tr_poll_error",
+                          "tr_clear_error", "tr_set_flag_timeout_ms", "tr_version",
+                          "tr_kernel_count", "tr_kernel_name", "tr_last_error"])
 
 
 def test_library_exports_every_declared_symbol(lib):
@@ -48,9 +49,37 @@ def test_library_exports_every_declared_symbol(lib):
         assert re.search(rf"\bT {name}\b", out), name
 
 
-def test_version_and_probe(lib):
-    assert b"sm_100a" in lib.lib().tr_version()
-    assert lib.lib().tr_kernel_count() >= 5
+def _cubin_kernels(path):
+    """Base names of the __global__ functions in a library's sm_100a cubin."""
+    sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+    names = set()
+    for mangled in re.findall(r"Function : (\S+)", sass):
+        dem = subprocess.run(["c++filt", mangled], capture_output=True, text=True).stdout.strip()
+        base = re.sub(r"<.*", "", dem.split("(")[0])
+        names.add(base.split("::")[-1])
+    return names
+
+
+def test_version_and_kernel_table(lib):
+    """tr_kernel_count / tr_kernel_name list exactly the kernels the cubin holds."""
+    L = lib.lib()
+    assert b"sm_100a" in L.tr_version()
+    n = L.tr_kernel_count()
+    table = {L.tr_kernel_name(i).decode() for i in range(n)}
+    assert len(table) == n and L.tr_kernel_name(n) is None and L.tr_kernel_name(-1) is None
+    cubin = _cubin_kernels(lib.LIB_PATH)
+    if not cubin:
+        pytest.skip("cuobjdump unavailable")
+    assert table == cubin
+
+
+def test_product_library_has_no_runtime_switches(lib):
+    """No kernel-selection switch in the product library (no backend
+    env switch; the CUDA runtime linked into it still reads its own variables),
+    and none of the rejected variants' kernels (checked by the kernel table)."""
+    strings = open(lib.LIB_PATH, "rb").read()
+    for switch in (b"TR_ATTN_PAIR2", b"TR_ATTN_PSMEM", b"TR_ATTN_PERSISTENT", b"TOKENRING_LIB"):
+        assert switch not in strings, switch
 
 
 def test_validation_maps_to_reference_errors(lib):

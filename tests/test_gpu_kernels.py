@@ -283,7 +283,9 @@ import sys
 import numpy as np, torch
 sys.path.insert(0, {root!r})
 from oracle import kernels as ok, splitmix
-from paper_2412_20501_b200 import kernels as K
+from paper_2412_20501_b200 import _lib, kernels as K
+if {lib!r}:
+    _lib.use_library({lib!r})
 worst_o = worst_l = 0.0
 for tq, tk, h, mask, qo, ko in [(256, 256, 2, 2, 0, 0), (512, 1024, 3, 0, 0, 0),
                                 (1000, 1000, 2, 2, 0, 0), (129, 257, 1, 2, 128, 0)]:
@@ -305,19 +307,25 @@ print(worst_o, worst_l)
 
 
 def test_single_cta_kernel_d128_subprocess(tmp_path):
-    """D=128 runs on the CTA-pair kernel by default; the single-CTA kernel it is
-    built from (TR_ATTN_PAIR2=0, chosen once per process) keeps its parity, and
-    the two agree closely (same MMA K order and softmax; they differ only in
-    which exp2 pairs go through the polynomial: 1 in 8 vs 1 in 6)."""
+    """D=128 runs on the CTA-pair kernel (the product library); the single-CTA
+    kernel it is built from (the experiments build with TR_ATTN_PAIR2=0 -- the
+    product has no run-time kernel switch) keeps its parity, and the two
+    agree closely (same MMA K order and softmax; they differ only in which
+    exp2 pairs go through the polynomial: 1 in 8 vs 1 in 6)."""
     import os
     import subprocess
     import sys
+    from paper_2412_20501_b200 import build
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not os.path.exists(build.EXP_LIB):
+        build.build(experiments=True)
     runs = {}
     for flag in ("0", "1"):
         out = str(tmp_path / f"pair{flag}")
         env = dict(os.environ, TR_ATTN_PAIR2=flag)
-        r = subprocess.run([sys.executable, "-c", _SINGLE_CTA_SCRIPT.format(root=root, out=out)],
+        lib = build.EXP_LIB if flag == "0" else ""
+        r = subprocess.run([sys.executable, "-c",
+                            _SINGLE_CTA_SCRIPT.format(root=root, out=out, lib=lib)],
                            env=env, capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
         worst_o, worst_l = map(float, r.stdout.split()[-2:])

@@ -46,7 +46,8 @@ def _port():
 SEEDS = (21, 22, 21)
 
 
-def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, nodes=1):
+def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, nodes=1,
+            schedule="token-ring"):
     """Back-to-back calls with different inputs and no host synchronisation
     in between (the runner's flags carry each call's initial conditions);
     rank 0 is delayed on the device before every call so its peers run ahead
@@ -59,7 +60,8 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, 
         from paper_2412_20501_b200 import rng
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
-                                    transport=transport, route=route, nodes=nodes)
+                                    transport=transport, route=route, nodes=nodes,
+                                    schedule=schedule)
         inputs = {sd: rng.local_inputs(sd, runner.part, rank, H, D) for sd in set(SEEDS)}
         outs = []
         for sd in SEEDS[:calls]:
@@ -84,15 +86,21 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, 
     (8, 8192, 2, 128, True, "direct", "fused"),
     # the multi-node hybrid schedule (KV rotated across "nodes" of 2 ranks)
     (4, 2048, 2, 128, False, "hybrid2", "ipc"), (4, 2048, 2, 128, False, "hybrid2", "fused"),
-    (6, 3072, 2, 64, False, "hybrid3", "fused")])
+    (6, 3072, 2, 64, False, "hybrid3", "fused"),
+    # Ring Attention (KV rotation, ref engine.py:203-230): the config-4 baseline
+    (2, 2048, 2, 128, True, "ringattn", "ipc"), (4, 4096, 2, 128, True, "ringattn", "ipc"),
+    (4, 2048, 2, 128, False, "ringattn", "fused"), (8, 8192, 2, 128, True, "ringattn", "fused"),
+    (3, 1536, 2, 64, True, "ringattn", "ipc")])
 def test_token_ring_ipc(world, S, H, D, causal, route, transport):
     ctx = mp.get_context("spawn")
     q_out = ctx.Queue()
     port = _port()
     nodes = int(route[6:]) if route.startswith("hybrid") else 1
-    route = "ring" if nodes > 1 else route
+    schedule = "ring" if route == "ringattn" else "token-ring"
+    route = "ring" if nodes > 1 or schedule == "ring" else route
     procs = [ctx.Process(target=_worker,
-                         args=(r, world, port, S, H, D, causal, 3, q_out, route, transport, nodes))
+                         args=(r, world, port, S, H, D, causal, 3, q_out, route, transport, nodes,
+                               schedule))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -104,7 +112,9 @@ def test_token_ring_ipc(world, S, H, D, causal, route, transport):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    if nodes > 1:
+    if schedule == "ring":
+        sched = osch.ring(world, S, H, D, causal)
+    elif nodes > 1:
         sched = osch.hybrid(nodes, world // nodes, S, H, D)
     else:
         sched = osch.zigzag_token_ring(world, S, H, D) if causal else osch.token_ring(world, S, H, D)

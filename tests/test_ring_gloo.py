@@ -39,7 +39,8 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring", nodes=1):
+def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring", nodes=1,
+            schedule="token-ring"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -47,7 +48,7 @@ def _worker(rank, world, port, S, H, D, causal, seed, result_q, route="ring", no
         from cpu_ops import OracleOps
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, ops=OracleOps(), device="cpu",
-                                    route=route, nodes=nodes)
+                                    route=route, nodes=nodes, schedule=schedule)
         q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(seed, S, H, D))
         rng = runner.part.ranges(rank)
         loc = [torch.as_tensor(opart.gather(x, rng), dtype=torch.float32).to(torch.bfloat16)
@@ -127,4 +128,44 @@ def test_hybrid_gloo(nodes, per_node, S):
     g_out, g_lse = opart.reorder([res[r][0] for r in range(world)],
                                  [res[r][1] for r in range(world)], osch.ranges_of(sched, S), S)
     d_out, d_lse = ok.dense_attention(q, k, v, False)
+    assert ok.max_relative_error(g_out, g_lse, d_out, d_lse) <= 2e-2
+
+
+@pytest.mark.parametrize("world,S,causal", [(2, 64, True), (4, 128, True), (3, 48, False),
+                                            (4, 64, False), (5, 80, True)])
+def test_ring_attention_gloo(world, S, causal):
+    """Ring Attention (KV rotation, ref engine.py:203-230) -- the config-4
+    baseline -- on the multi-process runner: contiguous shards, KV blocks
+    forwarded to rank+1 every step into the receiver's alternate KV store,
+    the causal ring's fully-masked blocks skipped; per rank equal to the
+    oracle's execute of the same schedule and, reassembled, to dense
+    attention."""
+    H, D = 2, 8
+    ctx = mp.get_context("spawn")
+    q_ = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, S, H, D, causal, 17, q_, "ring", 1, "ring"))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    _reap.extend(procs)
+    res = {}
+    for _ in range(world):
+        r, o, l = q_.get(timeout=120)
+        res[r] = (o, l)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(17, S, H, D))
+    sched = osch.ring(world, S, H, D, causal)
+    ref = osch.execute(sched, q, k, v)
+    for r in range(world):
+        assert np.abs(res[r][0] - ref[r][0]).max() <= 2e-2
+        fin = np.isfinite(ref[r][1])
+        assert np.array_equal(np.isfinite(res[r][1]), fin)
+        assert np.abs(res[r][1][fin] - ref[r][1][fin]).max() <= 1e-3
+    g_out, g_lse = opart.reorder([res[r][0] for r in range(world)],
+                                 [res[r][1] for r in range(world)], osch.ranges_of(sched, S), S)
+    d_out, d_lse = ok.dense_attention(q, k, v, causal)
     assert ok.max_relative_error(g_out, g_lse, d_out, d_lse) <= 2e-2
