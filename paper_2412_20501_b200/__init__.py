@@ -4,7 +4,7 @@ A drop-in for the attention path of the reference ``ringsim`` package
 (arxiv 2412.20501, "TokenRing"), with the same public names:
 
 * core:       MaskKind, MaskSpec, Partial, block_attention, merge_partial,
-              dense_attention, max_relative_error
+              dense_attention (alias dense_attention_oracle), max_relative_error
 * partition:  Partition, split_contiguous, split_zigzag, causal_work_count,
               gather_local, global_reorder
 * engine:     MsgKind, Schedule, build_ring_attention, build_token_ring,
@@ -25,7 +25,8 @@ from .partition import (Partition, causal_work_count, gather_local,  # noqa: F40
 
 from .kernels import BACKEND as KERNEL_BACKEND  # noqa: F401,E402
 from .core import (MaskKind, MaskSpec, Partial, block_attention,  # noqa: F401,E402
-                   dense_attention, max_relative_error, merge_partial)
+                   dense_attention, dense_attention_oracle, max_relative_error,
+                   merge_partial)
 from .engine import (MessageTrace, MsgKind, Schedule, build_ring_attention,  # noqa: F401,E402
                      build_hybrid, build_schedule, build_token_ring, build_zigzag_token_ring,
                      comm_volume,
@@ -33,4 +34,4 @@ from .engine import (MessageTrace, MsgKind, Schedule, build_ring_attention,  # n
 from .ring import TokenRingAttention, token_ring_attention  # noqa: F401,E402
 from . import core, engine, kernels, partition, ring, rng  # noqa: F401,E402
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

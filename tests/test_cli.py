@@ -103,3 +103,52 @@ def test_verify_profile_compare_on_gpu(tmp_path, capsys):
                      "ring,token-ring", "--sweep", "seq_len=64..128"]) == 0
     rows = capsys.readouterr().out.splitlines()
     assert rows[0] == cli.COMPARE_HEADER and len(rows) == 5
+
+
+def _reference_ringsim():
+    """The reference package (baseline/_ref install, else its source tree), or None."""
+    import importlib
+    import sys
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "ringsim")):
+            if path not in sys.path:
+                sys.path.append(path)
+            try:
+                return importlib.import_module("ringsim.cli"), importlib.import_module("ringsim.netsim")
+            except Exception:
+                return None
+    return None
+
+
+@pytest.mark.parametrize("cfg_name,override", [
+    ("a10_token_ring.json", None), ("a10_ring.json", None),
+    ("a10_token_ring.json", {"kind": "ring", "bandwidth_gbps": 50.0, "latency_us": 3.0}),
+    ("a10_ring.json", {"kind": "switch", "bandwidth_gbps": 900.0, "latency_us": 5.0}),
+    ("a10_ring.json", {"kind": "full-mesh", "bandwidth_gbps": 25.0, "latency_us": 5.0})])
+def test_modelled_comm_equals_reference_netsim(cfg_name, override):
+    """The modelled send/recv lanes equal the reference's netsim.simulate
+    (outbound / inbound per step and rank) on the reference's own configs --
+    including its fitted A10 matrix topology -- and on ring / switch /
+    full-mesh variants of them."""
+    ref = _reference_ringsim()
+    if ref is None:
+        pytest.skip("reference package not available")
+    rcli, rnet = ref
+    from paper_2412_20501_b200 import cli
+    path = os.path.join(ROOT, "configs", cfg_name)
+    if not os.path.exists(path):
+        path = os.path.join("/root/reference/pkg/configs", cfg_name)
+    if not os.path.exists(path):
+        pytest.skip("config not available")
+    data = json.load(open(path))
+    if override:
+        data["topology"] = override
+    mine = cli.RunConfig.from_dict(json.loads(json.dumps(data)))
+    theirs = rcli.RunConfig.from_dict(json.loads(json.dumps(data)))
+    send, recv = cli.modelled_comm(mine, cli.build_schedule(mine))
+    from ringsim.engine import trace_from_schedule
+    tl = rnet.simulate(trace_from_schedule(rcli.build_schedule(theirs)),
+                       rcli.build_topology(theirs), rcli.build_timing(theirs))
+    import numpy as np
+    assert np.allclose(np.array(send), tl.outbound, rtol=1e-12, atol=0)
+    assert np.allclose(np.array(recv), tl.inbound, rtol=1e-12, atol=0)
