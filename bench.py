@@ -17,10 +17,13 @@ inputs copied from pinned host memory and the output copied back inside the
 timed region.  Every q/k/v tensor is 1 GiB (> 126 MB L2), so no explicit L2
 flush is needed between steps.
 
-``--impl reference`` times the reference's own CPU kernels (oracle/_ref:
-ringsim/_kernels.pyx compiled from the reference sources, or the numpy port
-in oracle/ when it is absent) on the host cores on a bounded sample of the
-same workload and prints the same JSON line with "impl": "reference".
+``--impl reference`` times the reference's own CPU path -- its
+``engine.execute`` on the numpy backend (the faster one at scale, BASELINE.md
+section 3), from the unmodified install in baseline/_ref, or the oracle port
+when that is absent -- on all host cores, one head per process, on a bounded
+sample of the same schedule (S=16384, 8 simulated ranks), extrapolated to
+the full workload, and prints the same JSON line with "impl": "reference"
+(plus the reference's Cython kernels on causal row windows beside it).
 """
 
 import argparse
@@ -151,33 +154,130 @@ def reference_kind():
     return "reference" if ref_kernels.load() is not None else "port"
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")     # pip --target install of /root/reference
+EXEC_SAMPLE_S = 16384                                # sequence of one sampled execute
+EXEC_SAMPLE_P = 8                                    # simulated ranks (config 3's schedule)
+
+
+def _ref_package_ok():
+    return os.path.isdir(os.path.join(REF_PKG, "ringsim"))
+
+
+def _exec_sample_worker(args):
+    """One worker: the reference's own executor (``ringsim.engine.execute``,
+    ref engine.py:468-638) on its numpy backend (``RINGSIM_KERNELS=python``,
+    _kernels_ref.py) over the schedule of the benchmarked workload at H=1,
+    S=EXEC_SAMPLE_S, repeated with fresh inputs (one head each -- heads are
+    independent) until ``budget`` seconds of execute time.  Without the
+    reference install, the oracle port's execute (oracle/schedule.py).
+    Returns (algorithmic flops, seconds inside execute, executes)."""
+    schedule, causal, S, P, D, budget, seed = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["RINGSIM_KERNELS"] = "python"
+    if _ref_package_ok():
+        sys.path.insert(0, REF_PKG)
+        from ringsim import engine, rng
+        if schedule == "ring":
+            sched = engine.build_ring_attention(P, S, 1, D, causal=causal)
+        elif causal:
+            sched = engine.build_zigzag_token_ring(P, S, 1, D)
+        else:
+            sched = engine.build_token_ring(P, S, 1, D)
+        flops = sum(c.flops for c in engine.trace_from_schedule(sched).computes)
+
+        def run(sd):
+            q, k, v = rng.attention_inputs(sd, S, 1, D)
+            t = time.perf_counter()
+            engine.execute(sched, q, k, v)
+            return time.perf_counter() - t
+    else:
+        from oracle import schedule as osch
+        from oracle import splitmix
+        sched = (osch.ring(P, S, 1, D, causal) if schedule == "ring" else
+                 osch.zigzag_token_ring(P, S, 1, D) if causal else osch.token_ring(P, S, 1, D))
+        flops = osch.flops(sched, 1, D)
+
+        def run(sd):
+            q, k, v = splitmix.attention_inputs(sd, S, 1, D)
+            t = time.perf_counter()
+            osch.execute(sched, q, k, v)
+            return time.perf_counter() - t
+    busy, n = 0.0, 0
+    while True:
+        busy += run(seed + n)
+        n += 1
+        if busy >= budget:
+            return flops * n, busy, n
+
+
+def cpu_exec_rate(schedule, causal, D, budget_s=8.0, workers=None):
+    """Aggregate CPU TFLOP/s of the reference's CPU path on this host: every
+    core runs the reference's own ``execute`` of the benchmarked schedule
+    (8 simulated ranks, one head per execute) -- a bounded sample of the same
+    workload; the numpy backend's rate is flat in S (measured 18.0 / 18.2
+    GFLOP/s per core at S=16384 / 32768), so it extrapolates to the full one."""
+    import multiprocessing as mpc
+    workers = workers or len(os.sched_getaffinity(0))
+    ctx = mpc.get_context("spawn")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_exec_sample_worker,
+                       [(schedule, causal, EXEC_SAMPLE_S, EXEC_SAMPLE_P, D, budget_s, 1000 + 97 * i)
+                        for i in range(workers)])
+    wall = time.perf_counter() - t0
+    flops = sum(r[0] for r in res)
+    busy = max(r[1] for r in res)
+    return {"flops": flops, "seconds": busy, "wall": wall, "workers": workers,
+            "executes": sum(r[2] for r in res), "tflops": flops / busy / 1e12,
+            "kind": "reference" if _ref_package_ok() else "port"}
+
+
+def _exec_sample_text(r, a):
+    what = ("the reference package's own engine.execute (baseline/_ref, RINGSIM_KERNELS=python: "
+            "numpy/OpenBLAS, 1 BLAS thread per process)" if r["kind"] == "reference" else
+            "the oracle port's execute (oracle/schedule.py, numpy; reference install absent)")
+    sched = ("build_ring_attention" if a.schedule == "ring" else
+             "build_token_ring" if a.non_causal else "build_zigzag_token_ring")
+    return (f"{r['workers']} processes, each running {what} of {sched}({EXEC_SAMPLE_P}, "
+            f"{EXEC_SAMPLE_S}, 1, {a.head_dim}) on fresh one-head inputs: {r['executes']} executes "
+            f"in {r['seconds']:.1f} s; aggregate throughput extrapolated to the full workload "
+            f"(S={a.seq}, H={a.heads})")
+
+
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     S, H, D = a.seq, a.heads, a.head_dim
-    kind = reference_kind()
-    total = causal_flops(S, H, D)
+    total = workload_flops(a)
     rates = []
     for i in range(a.warmup + a.steps):
-        r = cpu_rate(kind, S, D, budget_s=2.0)
+        r = cpu_exec_rate(a.schedule, not a.non_causal, D, budget_s=2.0 if i < a.warmup else 6.0)
         if i >= a.warmup:
             rates.append(r)
     tflops = statistics.median(r["tflops"] for r in rates)
     sec_per_step = total / (tflops * 1e12)
     r0 = rates[0]
-    sample = (f"{r0['workers']} processes x 1 head, {r0['rows']} causal query rows (windows near the end "
-              f"of S={S} (keys 0..S), D={D}; {a.steps} timed samples; throughput extrapolated "
-              f"to the full workload ({total:.4e} flops)")
+    # the reference's other backend (Cython, compiled from its own source by
+    # oracle/Makefile) on causal row windows, for comparison
+    cy = None
+    if reference_kind() == "reference" and not a.non_causal:
+        c = cpu_rate("reference", S, D, budget_s=6.0)
+        cy = {"value": c["tflops"], "unit": "TFLOP/s", "cores": c["workers"],
+              "sample": f"ringsim/_kernels.pyx attention_block on {c['rows']} causal query rows "
+                        f"(8-row windows near the end of S={S}), {c['seconds']:.1f} s",
+              "faster_backend": "numpy execute" if tflops >= c["tflops"] else "cython kernels"}
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOP/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform[-1,1) fp64)",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 uniform[-1,1) fp64)",
         "config": workload_config(a, a.gpus),
         "tokens_per_s": S / sec_per_step,
         "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": r0["workers"],
-                         "kind": kind, "sample": sample},
+                         "kind": r0["kind"], "path": "engine.execute (numpy backend)",
+                         "extrapolated": True, "sample": _exec_sample_text(r0, a)},
+        "cpu_baseline_cython": cy,
         "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -542,13 +642,11 @@ def run_ours(a):
             "clocks": clk.summary(),
         }
         if not a.no_cpu_baseline:
-            kind = reference_kind()
-            r = cpu_rate(kind, S, D, budget_s=12.0)
+            r = cpu_exec_rate(a.schedule, causal, D, budget_s=10.0)
             line["cpu_baseline"] = {
-                "value": r["tflops"], "unit": "TFLOP/s", "cores": r["workers"], "kind": kind,
-                "sample": f"{r['workers']} processes x 1 head, {r['rows']} causal query rows (windows near "
-                          f"the end of S={S} (keys 0..S), D={D}, {r['seconds']:.1f} s; "
-                          "throughput of the reference's CPU kernels on this host"}
+                "value": r["tflops"], "unit": "TFLOP/s", "cores": r["workers"], "kind": r["kind"],
+                "path": "engine.execute (numpy backend)", "extrapolated": True,
+                "sample": _exec_sample_text(r, a)}
         print(json.dumps(line), flush=True)
     if world > 1:
         for r in runners:
