@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--non-causal", action="store_true",
                     help="non-causal attention (config-4 sweep; TokenRing then uses the "
                          "contiguous partition)")
+    ap.add_argument("--trace-out", default=None, metavar="PREFIX",
+                    help="after the timed steps, one more forward with every rank's lanes "
+                         "measured: PREFIX.json (Chrome trace, the reference's schema), PREFIX.csv "
+                         "(the reference's step CSV), PREFIX_exchange.json")
     ap.add_argument("--transport", default="fused", choices=["nccl", "ipc", "fused"],
                     help="N>1 exchange: fused (default: Q by copy engines into the peer's "
                          "IPC-mapped buffer, OUT rows stored by the attention epilogue straight "
@@ -583,6 +587,31 @@ def run_ours(a):
     attn_avg_ms = kern_ms / max(1, nlaunch)
     attn_flops_per_launch = kern_flops / max(1, nlaunch)
     exposed, attn_avg_ms = allmax([exposed, attn_avg_ms])
+
+    if a.trace_out:
+        from paper_2412_20501_b200 import timeline as tl_mod
+        barrier()
+        torch.cuda.synchronize()
+        origin = torch.cuda.Event(enable_timing=True)
+        origin.record()
+        runner(q, k, v)
+        torch.cuda.synchronize()
+        recs = tl_mod.rank_records(runner, origin)
+        if world > 1:
+            everyone = [None] * world
+            dist.all_gather_object(everyone, recs)
+        else:
+            everyone = [recs]
+        if rank == 0:
+            records = dict(enumerate(everyone))
+            os.makedirs(os.path.dirname(os.path.abspath(a.trace_out)), exist_ok=True)
+            with open(a.trace_out + ".json", "w") as f:
+                f.write(tl_mod.emit_chrome_trace(records))
+            with open(a.trace_out + ".csv", "w") as f:
+                f.write(tl_mod.summary_csv(records, runner.sched.kind, world, S, H, D))
+            with open(a.trace_out + "_exchange.json", "w") as f:
+                json.dump(dict(tl_mod.exchange_summary(records), transport=runner.transport,
+                               shared_device=shared, schedule=runner.sched.kind), f, indent=1)
 
     # end-to-end through the public API with host buffers
     e2e = None

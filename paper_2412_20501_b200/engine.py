@@ -654,6 +654,7 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list
             raise ScheduleError(f"step {last} rank {m[0]}: {m[2].value} message left in flight "
                                 "after the final step")
         fold(last, m[1], m)
+    del stage_out, stage_lse           # release the step buffers before the output copies
     outputs = {}
     for r in range(P):
         rng = sched.partition.ranges(r)

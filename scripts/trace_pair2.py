@@ -60,3 +60,19 @@ a1 = (t[list(range(8, 12))][:, J, 2].min(0), t[list(range(8, 12))][:, J, 4].max(
 ov = np.maximum(0, np.minimum(a0[1], a1[1]) - np.maximum(a0[0], a1[0]))
 ov2 = np.maximum(0, np.minimum(a0[1][1:], a1[1][:-1]) - np.maximum(a0[0][1:], a1[0][:-1]))
 print(f"exp-phase overlap of the halves (same tile / half0 j+1 vs half1 j): {med(ov):.0f} / {med(ov2):.0f}")
+# one tile's events in time order (relative to half 0's S ready of tile j0)
+j0 = 20
+base = t[4][j0, 1]
+evs = [("MMA K_j landed (iter start)", mma[j0, 0]), ("MMA V_j landed", mma[j0, 3]),
+       ("MMA QK0(j) issued", mma[j0, 7]), ("MMA QK1(j) issued", mma[j0, 6]),
+       ("MMA QK0(j+1) issued", mma[j0 + 1, 7]),
+       ("MMA sees P1(j-1) c0", mma[j0 - 1, 1]), ("MMA sees P1(j-1) c1", mma[j0 - 1, 2]),
+       ("MMA sees P0(j) c0", mma[j0, 4]), ("MMA sees P0(j) c1", mma[j0, 5]),
+       ("MMA sees P1(j) c0", mma[j0, 1]), ("MMA sees P1(j) c1", mma[j0, 2]),
+       ("MMA K_j+1 landed (next iter)", mma[j0 + 1, 0])]
+for w in (4, 5, 8, 9):
+    evs += [(f"w{w} S ready", t[w][j0, 1]), (f"w{w} max done", t[w][j0, 2]),
+            (f"w{w} c0 pub", t[w][j0, 3]), (f"w{w} c1 pub", t[w][j0, 4]),
+            (f"w{w} next S ready", t[w][j0 + 1, 1])]
+for name, x in sorted(evs, key=lambda e: e[1]):
+    print(f"  {int(x - base):7d}  {name}")

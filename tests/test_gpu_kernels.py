@@ -73,6 +73,11 @@ CASES = [
     (64, 64, 2, 128, 2, 0, 64),     # everything masked
     (200, 72, 2, 32, 0, 0, 0),      # CUDA-core kernel (D=32)
     (50, 70, 2, 8, 2, 20, 0),       # CUDA-core kernel (D=8)
+    # MASK_FULL (fully masked block): zeros / -inf without reading the inputs
+    # (ref _kernels_ref.py:37-38, tests/test_kernels.py:22-38)
+    (256, 384, 2, 128, 1, 0, 0),
+    (100, 64, 3, 64, 1, 5, 7),
+    (33, 17, 2, 32, 1, 0, 0),
 ]
 
 
@@ -99,6 +104,91 @@ def test_large_scores_rescale_path(K):
     out, lse = K.attention_block(dev(q), dev(k), dev(v), 0)
     torch.cuda.synchronize()
     check(out, lse, ref_out, ref_lse, "rescale")
+
+
+@pytest.mark.parametrize("d", [128, 64])
+def test_large_scores_stay_finite(K, d):
+    """The reference's |score| up to 700 case (pkg/tests/test_core.py:76-85)
+    on the tcgen05 kernels: q = 700 against keys +-1 along one head-dim
+    column (scores +-700/sqrt(D) after scaling, far past the lazy-rescale
+    threshold and the fp32 exp range without the max shift), and a 700x
+    version of random inputs; out and lse finite and within tolerance of
+    the float64 oracle.  Every row of both tiles sees the extremes."""
+    tq, tk, h = 256, 512, 2
+    q = np.zeros((tq, h, d))
+    q[:, :, 0] = 700.0
+    k = np.zeros((tk, h, d))
+    k[0::2, :, 0] = 1.0
+    k[1::2, :, 0] = -1.0
+    v = np.zeros((tk, h, d))
+    v[0::2] = 3.0
+    v[1::2] = -5.0
+    ro, rl = ok.attention_block(q, k, v, ok.MASK_NONE)
+    out, lse = K.attention_block(dev(q), dev(k), dev(v), 0)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
+    check(out, lse, ro, rl, f"700 d={d}")
+    # random directions scaled to |score| up to ~700 before the scale
+    qr, kr, vr = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(700 + d, tk, h, d))
+    sc = np.sqrt(300.0 / np.sqrt(d))        # raw q.k std ~100: extremes of several hundred
+    qr = splitmix.to_bf16_f64(qr[:tq] * sc)
+    kr = splitmix.to_bf16_f64(kr * sc)
+    assert np.abs(np.einsum("qhd,khd->hqk", qr, kr)).max() > 300
+    ro, rl = ok.attention_block(qr, kr, vr, ok.MASK_CAUSAL, tk - tq, 0)
+    out, lse = K.attention_block(dev(qr), dev(kr), dev(vr), 2, tk - tq, 0)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
+    check(out, lse, ro, rl, f"700-random d={d}")
+
+
+def test_reference_700_case_literal(K):
+    """pkg/tests/test_core.py:76-85 verbatim in shape: q = 700, keys +-1,
+    values 3 / -5, D = 1 (the CUDA-core kernel's path)."""
+    q = np.full((2, 1, 1), 700.0)
+    k = np.array([[[1.0]], [[-1.0]]])
+    v = np.array([[[3.0]], [[-5.0]]])
+    ro, rl = ok.attention_block(q, k, v, ok.MASK_NONE)
+    out, lse = K.attention_block(dev(q), dev(k), dev(v), 0)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
+    check(out, lse, ro, rl, "700 literal")
+
+
+def test_misaligned_tensor_is_an_error_not_a_silent_fallback(K):
+    """D=128 tensors the TMA kernels cannot address (base not 16-byte
+    aligned) raise UnsupportedError instead of silently switching kernel."""
+    from paper_2412_20501_b200._lib import UnsupportedError
+    buf = torch.zeros(64 * 2 * 128 + 1, dtype=torch.bfloat16, device="cuda")
+    q = buf[1:].view(64, 2, 128)                   # 2-byte offset
+    k = torch.zeros(64, 2, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(UnsupportedError, match="aligned"):
+        K.attention_block(q, k, k, 0)
+
+
+def test_flag_wait_timeout_is_a_schedule_error(K):
+    """A message that never arrives: the device-side wait gives up after its
+    timeout (instead of trapping and killing the context), and the host
+    reports it as the reference's ScheduleError; the context stays usable."""
+    from paper_2412_20501_b200.errors import ScheduleError
+    flag = torch.zeros(1, dtype=torch.int64, device="cuda")
+    K.clear_error()
+    K.set_flag_timeout_ms(200)
+    try:
+        K.flag_wait_(flag, 5)
+        torch.cuda.synchronize()
+        with pytest.raises(ScheduleError, match="not delivered"):
+            K.poll_error()
+        K.clear_error()
+        K.poll_error()
+        K.flag_set_(flag, 5)
+        K.flag_wait_(flag, 5)
+        torch.cuda.synchronize()
+        K.poll_error()
+        x = torch.ones(4, device="cuda") * 2                # context still alive
+        assert float(x.sum()) == 8.0
+    finally:
+        K.set_flag_timeout_ms(30000)
+        K.clear_error()
 
 
 def test_segments_zigzag_step0(K):
