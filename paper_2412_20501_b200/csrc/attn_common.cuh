@@ -50,16 +50,21 @@ struct AttnCfg {
 // tr_debug_trace().  Not compiled into the product library.
 // CTAs 0 and 1 (a pair in the TR_KERNEL_PAIR build); slots 0-5 clock64,
 // slot 6-7 free; TR_TRACE_GT(slot) records %globaltimer (cross-SM).
-static __device__ unsigned long long g_trace[2 * 12 * 64 * 8];
+static __device__ unsigned long long g_trace[2 * 20 * 64 * 8];   // [CTA][warp < 20][tile][slot]
 #define TR_TRACE_AT(slot, jj)                                                        \
   do {                                                                               \
     if (blockIdx.x < 2 && lane == 0 && (jj) >= 0 && (jj) < 64)                                  \
-      g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = clock64();      \
+      g_trace[((blockIdx.x * 20 + warp) * 64 + (jj)) * 8 + (slot)] = clock64();      \
+  } while (0)
+#define TR_TRACE_W(w, slot, jj)                                                      \
+  do {                                                                               \
+    if (blockIdx.x < 2 && lane == 0 && (jj) >= 0 && (jj) < 64)                                  \
+      g_trace[((blockIdx.x * 20 + (w)) * 64 + (jj)) * 8 + (slot)] = clock64();       \
   } while (0)
 #define TR_TRACE_GT(slot, jj)                                                        \
   do {                                                                               \
     if (blockIdx.x < 2 && lane == 0 && (jj) >= 0 && (jj) < 64)                                  \
-      g_trace[((blockIdx.x * 12 + warp) * 64 + (jj)) * 8 + (slot)] = globaltimer_ns(); \
+      g_trace[((blockIdx.x * 20 + warp) * 64 + (jj)) * 8 + (slot)] = globaltimer_ns(); \
   } while (0)
 #else
 #define TR_TRACE_AT(slot, jj) \
@@ -67,6 +72,9 @@ static __device__ unsigned long long g_trace[2 * 12 * 64 * 8];
   } while (0)
 #define TR_TRACE_GT(slot, jj) \
   do {                        \
+  } while (0)
+#define TR_TRACE_W(w, slot, jj) \
+  do {                          \
   } while (0)
 #endif
 

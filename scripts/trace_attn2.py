@@ -31,12 +31,12 @@ for _ in range(3):
     K.attention_block(q, k, v, 0)
 torch.cuda.synchronize()
 CTA = int(os.environ.get("CTA", "0"))      # 1: the second CTA of a pair build
-buf = np.zeros(2 * 12 * 64 * 8, dtype=np.uint64)
+buf = np.zeros(2 * 20 * 64 * 8, dtype=np.uint64)
 L = _lib.lib()
 fn = getattr(L, os.environ.get("TRACE_SYM", "tr_debug_trace"))   # tr_debug_trace_pair2: pair build
 fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert fn(buf.ctypes.data, buf.nbytes) == 0
-t_all = buf.reshape(2, 12, 64, 8).astype(np.int64)
+t_all = buf.reshape(2, 20, 64, 8).astype(np.int64)
 t = t_all[CTA]
 if CTA:   # softmax events of CTA 1 against the leader's MMA warp (cluster-local clocks differ)
     t = t.copy()

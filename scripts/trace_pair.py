@@ -20,11 +20,11 @@ v = torch.randn(tk, h, d, device="cuda").to(torch.bfloat16)
 for _ in range(3):
     K.attention_block(q, k, v, 0)
 torch.cuda.synchronize()
-buf = np.zeros(2 * 12 * 64 * 8, dtype=np.uint64)
+buf = np.zeros(2 * 20 * 64 * 8, dtype=np.uint64)
 L = _lib.lib()
 L.tr_debug_trace_variants.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert L.tr_debug_trace_variants(buf.ctypes.data, buf.nbytes) == 0
-t = buf.reshape(2, 12, 64, 8).astype(np.int64)
+t = buf.reshape(2, 20, 64, 8).astype(np.int64)
 J = slice(8, 60)
 MW = int(os.environ.get("MMA_WARP", 1))
 mma = t[0, MW]

@@ -27,11 +27,11 @@ v = torch.randn(tk, h, d, device="cuda").to(torch.bfloat16)
 for _ in range(3):
     K.attention_block(q, k, v, 0)
 torch.cuda.synchronize()
-buf = np.zeros(2 * 12 * 64 * 8, dtype=np.uint64)
+buf = np.zeros(2 * 20 * 64 * 8, dtype=np.uint64)
 L = _lib.lib()
 L.tr_debug_trace_pair2.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert L.tr_debug_trace_pair2(buf.ctypes.data, buf.nbytes) == 0
-t = buf.reshape(2, 12, 64, 8).astype(np.int64)[0]      # CTA 0
+t = buf.reshape(2, 20, 64, 8).astype(np.int64)[0]      # CTA 0
 J = np.arange(8, 56)
 mma = t[1]
 med = lambda x: float(np.median(x))  # noqa: E731
@@ -65,7 +65,9 @@ j0 = 20
 base = t[4][j0, 1]
 evs = [("MMA K_j landed (iter start)", mma[j0, 0]), ("MMA V_j landed", mma[j0, 3]),
        ("MMA QK0(j) issued", mma[j0, 7]), ("MMA QK1(j) issued", mma[j0, 6]),
-       ("MMA QK0(j+1) issued", mma[j0 + 1, 7]),
+       ("MMA QK0(j+1) issued", mma[j0 + 1, 7]), ("MMA PV0(j) c1 issued", t[2][j0, 0]),
+       ("TMA K_j+1 load issued", t[0][j0 + 1, 0]), ("TMA V_j+1 load issued", t[0][j0 + 1, 1]),
+       ("TMA K_j+2 load issued", t[0][j0 + 2, 0]), ("TMA K_j+3 load issued", t[0][j0 + 3, 0]),
        ("MMA sees P1(j-1) c0", mma[j0 - 1, 1]), ("MMA sees P1(j-1) c1", mma[j0 - 1, 2]),
        ("MMA sees P0(j) c0", mma[j0, 4]), ("MMA sees P0(j) c1", mma[j0, 5]),
        ("MMA sees P1(j) c0", mma[j0, 1]), ("MMA sees P1(j) c1", mma[j0, 2]),

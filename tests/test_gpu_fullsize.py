@@ -72,7 +72,7 @@ def test_config3_zigzag_p8_full_size():
     assert sum(c.flops for c in trace.computes) == 140738562097152
     # every head, >= 64 rows each (chunk edges of all 16 zigzag chunks + random)
     c = S // (2 * P)
-    rows = sorted(set(_rows(S, c, 1, n_random=24) + [a * c + e for a in range(2 * P)
+    rows = sorted(set(_rows(S, c, 1, n_random=40) + [a * c + e for a in range(2 * P)
                                                        for e in (0, c - 1)]))
     assert len(rows) >= 64
     _check_rows(q, k, v, merged.out, merged.lse, rows, range(H))
