@@ -444,16 +444,20 @@ def exchange_report(world, runner, xsum, n_fwd, shared):
     """Per-direction exchange of the TokenRing schedule (Q
     forward, OUT_LSE reverse) in GB/s against NVLink 5's 900 GB/s per
     direction.  Bytes are algorithmic (Q: rows*H*D*2, OUT: rows*H*(2D+4)),
-    summed over all ranks; time is the device time of the transfers."""
+    summed over all ranks; time is the device time of the transfers.  The
+    Ring-Attention baseline moves KV blocks instead (rows*H*D*2*2 per hop)."""
     if world == 1:
         return None
-    q_b, q_ms, o_b, o_ms = xsum
+    q_b, q_ms, o_b, o_ms, k_b, k_ms = xsum
     fwd = max(1, n_fwd)
     rep = {"peak_gbs_per_direction": 900.0,
            "q_bytes_per_forward": q_b / fwd, "out_bytes_per_forward": o_b / fwd,
            "q_gbs": q_b / (q_ms * 1e-3) / 1e9 if q_ms > 0 else None,
            "out_gbs": o_b / (o_ms * 1e-3) / 1e9 if o_ms > 0 else None,
            "transport": runner.transport}
+    if k_b > 0:
+        rep["kv_bytes_per_forward"] = k_b / fwd
+        rep["kv_gbs"] = k_b / (k_ms * 1e-3) / 1e9 if k_ms > 0 else None
     if runner.transport == "fused":
         rep["out_path"] = ("epilogue stores into the home's slot; out_gbs = bytes over the "
                            "launch that computes them (link load, not link peak)")
@@ -570,19 +574,22 @@ def run_ours(a):
     # exchange: copy-engine transfers timed on the copy stream (ipc: Q and
     # OUT; fused: Q, while OUT rides inside the attention launch that
     # computes it, so its rate is the bytes over that launch's time)
-    xq_b = xq_ms = xo_b = xo_ms = 0.0
+    xq_b = xq_ms = xo_b = xo_ms = xk_b = xk_ms = 0.0
     for tl in timelines:
         for ev in tl:
             for e0, e1, nb in ev.get("q_copies", ()):
                 xq_b += nb
                 xq_ms += e0.elapsed_time(e1)
+            for e0, e1, nb in ev.get("kv_copies", ()):   # ring / hybrid: KV rotation
+                xk_b += nb
+                xk_ms += e0.elapsed_time(e1)
             for e0, e1, nb in ev.get("o_copies", ()):
                 xo_b += nb
                 xo_ms += e0.elapsed_time(e1)
             if "o_push_bytes" in ev:
                 xo_b += ev["o_push_bytes"]
                 xo_ms += ev["attn_start"].elapsed_time(ev["attn_end"])
-    xsum = allsum([xq_b, xq_ms, xo_b, xo_ms])
+    xsum = allsum([xq_b, xq_ms, xo_b, xo_ms, xk_b, xk_ms])
     exposed = stall / max(1, len(timelines))
     attn_avg_ms = kern_ms / max(1, nlaunch)
     attn_flops_per_launch = kern_flops / max(1, nlaunch)

@@ -54,6 +54,12 @@ for half, ws, seen0, seen1 in ((0, range(4, 8), 4, 5), (1, range(8, 12), 1, 2)):
     per_warp = [f"w{w}: max {med(t[w][J, 2] - t[w][J, 1]):.0f} c0 {med(t[w][J, 3] - t[w][J, 2]):.0f} "
                 f"c1 {med(t[w][J, 4] - t[w][J, 3]):.0f}" for w in ws]
     print("   " + " | ".join(per_warp))
+    if sw[:, J, 7].min() > 0:     # builds with the chunk-computed marks
+        ex0 = sw[:, J, 7]
+        print(f"   max->exp start {med(ex0.max(0) - mx):.0f} | exp c0 {med((sw[:, J, 5] - ex0).max(0)):.0f} "
+              f"store+arrive c0 {med((sw[:, J, 3] - sw[:, J, 5]).max(0)):.0f} | exp c1 "
+              f"{med((sw[:, J, 6] - sw[:, J, 3]).max(0)):.0f} store+arrive c1 "
+              f"{med((sw[:, J, 4] - sw[:, J, 6]).max(0)):.0f}")
 # overlap of the two halves' exp phases: [max done, c1 published] intervals
 a0 = (t[list(range(4, 8))][:, J, 2].min(0), t[list(range(4, 8))][:, J, 4].max(0))
 a1 = (t[list(range(8, 12))][:, J, 2].min(0), t[list(range(8, 12))][:, J, 4].max(0))
