@@ -63,6 +63,10 @@ def parse():
                     help="after the timed steps, one more forward with every rank's lanes "
                          "measured: PREFIX.json (Chrome trace, the reference's schema), PREFIX.csv "
                          "(the reference's step CSV), PREFIX_exchange.json")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="time CUDA-graph replays of the forward (TokenRingAttention.capture); "
+                         "default on for N>1 with the ipc/fused transports")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--transport", default="fused", choices=["nccl", "ipc", "fused"],
                     help="N>1 exchange: fused (default: Q by copy engines into the peer's "
                          "IPC-mapped buffer, OUT rows stored by the attention epilogue straight "
@@ -532,19 +536,29 @@ def run_ours(a):
         if world > 1:
             dist.barrier()
 
+    host_ms = [0.0]
+
     def timed(fn, steps):
         barrier()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
+        h0 = time.perf_counter()
         for _ in range(steps):
             fn()
+        # host time to enqueue the steps (no sync inside): when it exceeds the
+        # device time the GPU waits on the host
+        host_ms[0] = (time.perf_counter() - h0) * 1e3 / steps
         e.record()
         torch.cuda.synchronize()
         barrier()
         return allmax([s.elapsed_time(e) / steps])[0]
 
     timelines = []
+
+    # CUDA-graph replay of the whole forward (TokenRingAttention.capture): one
+    # graph launch of host work per step instead of the step loop's launches
+    use_graph = a.graph if a.graph is not None else (world > 1 and transport in ("ipc", "fused"))
 
     def step():
         runner(q, k, v)
@@ -553,11 +567,30 @@ def run_ours(a):
     for _ in range(a.warmup):
         step()
     timelines.clear()
+    launches_per_step = None
+    if use_graph:
+        l0 = kernels.LAUNCHES
+        runner(q, k, v)                        # one eager forward: count its launches
+        launches_per_step = kernels.LAUNCHES - l0
+        runner.record_timeline = False
+        runner.capture(q, k, v, warmup=1)
+        timelines.clear()
     launches0 = kernels.LAUNCHES
     with ClockSampler(dev_index) as clk:
         ms = timed(step, a.steps)
-    launches = (kernels.LAUNCHES - launches0) // a.steps * a.steps
+    host_enqueue_ms = allmax([host_ms[0]])[0]
+    launches = ((kernels.LAUNCHES - launches0) // a.steps * a.steps if launches_per_step is None
+                else launches_per_step * a.steps)
     torch.cuda.synchronize()
+    if use_graph:
+        # the per-step lanes (exposed comm, kernel time, exchange) from eager
+        # forwards with CUDA events, after the timed replays
+        timelines.clear()
+        runner.record_timeline = True
+        for _ in range(2):
+            runner._forward(q, k, v)
+            timelines.append(runner.timeline)
+        torch.cuda.synchronize()
 
     # exposed comm (stall of the compute stream on comm events) and the
     # attention kernel's own device time, from the per-step CUDA events
@@ -601,7 +634,7 @@ def run_ours(a):
         torch.cuda.synchronize()
         origin = torch.cuda.Event(enable_timing=True)
         origin.record()
-        runner(q, k, v)
+        runner._forward(q, k, v)           # eager, with its per-stream events
         torch.cuda.synchronize()
         recs = tl_mod.rank_records(runner, origin)
         if world > 1:
@@ -663,6 +696,8 @@ def run_ours(a):
                               if shared else {})),
             "tokens_per_s": S / (ms * 1e-3),
             "exposed_comm_ms_per_step": exposed,
+            "host_enqueue_ms_per_step": host_enqueue_ms,
+            "cuda_graph": bool(use_graph),
             "exchange": exchange_report(world, runner, xsum, len(timelines), shared),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,

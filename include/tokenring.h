@@ -101,6 +101,13 @@ int tr_attention_segments_push(const void* q, const void* k, const void* v, void
                                int32_t n_kv, int32_t causal, int64_t row_shift, int64_t lse_stride,
                                uint32_t* done_count, uint64_t* done_flag, uint64_t done_value,
                                void* stream);
+int tr_attention_segments_push_rel(const void* q, const void* k, const void* v, void* out,
+                                   float* lse, int64_t tq_total, int64_t tk_total, int32_t heads,
+                                   int32_t head_dim, const tr_segment* q_segs, int32_t n_q,
+                                   const tr_segment* kv_segs, int32_t n_kv, int32_t causal,
+                                   int64_t row_shift, int64_t lse_stride, uint32_t* done_count,
+                                   uint64_t* done_flag, const int64_t* done_epoch,
+                                   int64_t done_offset, void* stream);
 
 /* kernels.merge_state, in place on a float32 accumulator:
  *   acc <- merge(acc, blk)     (ref _kernels.pyx:68-102)
@@ -142,6 +149,15 @@ int tr_splitmix_bf16(uint64_t seed, int64_t first, int64_t count, double low, do
  * engine.execute (pkg/src/ringsim/engine.py:515-518, 595-619). */
 int tr_flag_set(uint64_t* flag, uint64_t value, void* stream);
 int tr_flag_wait(const uint64_t* flag, uint64_t value, void* stream);
+/* Epoch-relative forms for CUDA-graph replay: the value is *epoch + offset,
+ * read on the device when the operation runs (epoch: a device int64 of the
+ * caller), and tr_epoch_add(epoch, delta) advances it at the end of a
+ * captured forward -- a replayed graph then uses fresh sequence values without
+ * any host work.  tr_attention_segments_push_rel raises done_flag to
+ * *done_epoch + done_offset. */
+int tr_flag_set_rel(uint64_t* flag, const int64_t* epoch, int64_t offset, void* stream);
+int tr_flag_wait_rel(const uint64_t* flag, const int64_t* epoch, int64_t offset, void* stream);
+int tr_epoch_add(int64_t* epoch, int64_t delta, void* stream);
 int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 /* Let kernels of the calling thread's current device load/store memory of
  * peer_device (flags, receive slots mapped over CUDA IPC): wraps

@@ -55,8 +55,6 @@ int launch_partial_init(float* acc_out, float* acc_lse, int64_t T, int H, int D,
 int launch_fill(float* p, int64_t n, float v, cudaStream_t s);
 int launch_splitmix(uint64_t seed, int64_t first, int64_t count, double low, double high,
                     void* dst, cudaStream_t s);
-int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s);
-int launch_flag_wait(const unsigned long long* flag, unsigned long long value, cudaStream_t s);
 
 static int check_segments(const tr_segment* segs, int n, int64_t total, const char* what) {
   if (n < 0 || n > TR_MAX_SEGMENTS)
@@ -116,6 +114,7 @@ struct PushOpts {
   unsigned int* done_count = nullptr;
   unsigned long long* done_flag = nullptr;
   unsigned long long done_value = 0;
+  const long long* done_epoch = nullptr;
 };
 
 static int run_segments(const void* q, const void* k, const void* v, void* out, float* lse,
@@ -138,7 +137,8 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
     if (ks[i].rows > 0) plan.kv[plan.nkv++] = ks[i];
   // a pushing launch with nothing to compute still owes its receiver the flag
   auto flag_only = [&]() {
-    return push.done_flag ? launch_flag_set(push.done_flag, push.done_value, s) : TR_OK;
+    return push.done_flag ? launch_flag_set(push.done_flag, push.done_value, s, push.done_epoch)
+                          : TR_OK;
   };
   if (plan.nq == 0) return flag_only();
   plan.causal = causal ? 1 : 0;
@@ -158,6 +158,7 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   plan.done_count = push.done_count;
   plan.done_flag = push.done_flag;
   plan.done_value = push.done_value;
+  plan.done_epoch = push.done_epoch;
   plan.tile_prefix[0] = 0;
   for (int i = 0; i < plan.nq; ++i)
     plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
@@ -212,12 +213,12 @@ int tr_attention_segments(const void* q, const void* k, const void* v, void* out
                       n_kv, causal, out_dtype, static_cast<cudaStream_t>(stream));
 }
 
-int tr_attention_segments_push(const void* q, const void* k, const void* v, void* out, float* lse,
+static int segments_push(const void* q, const void* k, const void* v, void* out, float* lse,
                                int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
                                const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
                                int32_t n_kv, int32_t causal, int64_t row_shift, int64_t lse_stride,
                                uint32_t* done_count, uint64_t* done_flag, uint64_t done_value,
-                               void* stream) {
+                               const int64_t* done_epoch, void* stream) {
   if (!out || !lse) return fail(TR_ERR_INPUT, "null out/lse");
   if (row_shift < 0 || lse_stride < 1) return fail(TR_ERR_DIMENSION, "row_shift >= 0, lse_stride >= 1 required");
   if ((done_flag == nullptr) != (done_count == nullptr))
@@ -231,8 +232,33 @@ int tr_attention_segments_push(const void* q, const void* k, const void* v, void
   push.done_count = done_count;
   push.done_flag = reinterpret_cast<unsigned long long*>(done_flag);
   push.done_value = done_value;
+  push.done_epoch = reinterpret_cast<const long long*>(done_epoch);
   return run_segments(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
                       n_kv, causal, TR_DTYPE_BF16, static_cast<cudaStream_t>(stream), push);
+}
+
+int tr_attention_segments_push(const void* q, const void* k, const void* v, void* out, float* lse,
+                               int64_t tq_total, int64_t tk_total, int32_t heads, int32_t head_dim,
+                               const tr_segment* q_segs, int32_t n_q, const tr_segment* kv_segs,
+                               int32_t n_kv, int32_t causal, int64_t row_shift, int64_t lse_stride,
+                               uint32_t* done_count, uint64_t* done_flag, uint64_t done_value,
+                               void* stream) {
+  return segments_push(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
+                       n_kv, causal, row_shift, lse_stride, done_count, done_flag, done_value,
+                       nullptr, stream);
+}
+
+int tr_attention_segments_push_rel(const void* q, const void* k, const void* v, void* out,
+                                   float* lse, int64_t tq_total, int64_t tk_total, int32_t heads,
+                                   int32_t head_dim, const tr_segment* q_segs, int32_t n_q,
+                                   const tr_segment* kv_segs, int32_t n_kv, int32_t causal,
+                                   int64_t row_shift, int64_t lse_stride, uint32_t* done_count,
+                                   uint64_t* done_flag, const int64_t* done_epoch,
+                                   int64_t done_offset, void* stream) {
+  if (!done_epoch) return fail(TR_ERR_INPUT, "null epoch");
+  return segments_push(q, k, v, out, lse, tq_total, tk_total, heads, head_dim, q_segs, n_q, kv_segs,
+                       n_kv, causal, row_shift, lse_stride, done_count, done_flag,
+                       static_cast<uint64_t>(done_offset), done_epoch, stream);
 }
 
 int tr_merge_state(float* acc_out, float* acc_lse, const void* blk_out, int32_t blk_dtype,
@@ -286,6 +312,26 @@ int tr_flag_wait(const uint64_t* flag, uint64_t value, void* stream) {
                           static_cast<cudaStream_t>(stream));
 }
 
+int tr_flag_set_rel(uint64_t* flag, const int64_t* epoch, int64_t offset, void* stream) {
+  if (!flag || !epoch) return fail(TR_ERR_INPUT, "null flag or epoch");
+  return launch_flag_set(reinterpret_cast<unsigned long long*>(flag),
+                         static_cast<unsigned long long>(offset), static_cast<cudaStream_t>(stream),
+                         reinterpret_cast<const long long*>(epoch));
+}
+
+int tr_flag_wait_rel(const uint64_t* flag, const int64_t* epoch, int64_t offset, void* stream) {
+  if (!flag || !epoch) return fail(TR_ERR_INPUT, "null flag or epoch");
+  return launch_flag_wait(reinterpret_cast<const unsigned long long*>(flag),
+                          static_cast<unsigned long long>(offset), static_cast<cudaStream_t>(stream),
+                          reinterpret_cast<const long long*>(epoch));
+}
+
+int tr_epoch_add(int64_t* epoch, int64_t delta, void* stream) {
+  if (!epoch) return fail(TR_ERR_INPUT, "null epoch");
+  return launch_epoch_add(reinterpret_cast<long long*>(epoch), delta,
+                          static_cast<cudaStream_t>(stream));
+}
+
 int tr_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
   if (bytes == 0) return TR_OK;
   if (!dst || !src) return fail(TR_ERR_INPUT, "null pointer");
@@ -324,7 +370,8 @@ static const char* const kKernels[] = {
     "merge_vec8_kernel",      "merge_scalar_kernel",   "merge_scalar_lse_kernel",
     "merge_n_vec8_kernel",    "merge_n_bf16_kernel",   "merge_n_scalar_kernel",
     "merge_n_lse_kernel",     "fill_kernel",
-    "flag_set_kernel",        "flag_wait_kernel",      "splitmix_bf16_kernel"};
+    "flag_set_kernel",        "flag_wait_kernel",      "epoch_add_kernel",
+    "splitmix_bf16_kernel"};
 
 const char* tr_version(void) { return "tokenring-b200 0.2 (sm_100a)"; }
 int32_t tr_kernel_count(void) { return int32_t(sizeof(kKernels) / sizeof(kKernels[0])); }

@@ -13,7 +13,19 @@
 
 namespace tr {
 
-__global__ void flag_set_kernel(unsigned long long* flag, unsigned long long value) {
+// `epoch` (optional, a device int64 of the caller): the value is relative,
+// *epoch + (signed) value, read when the kernel runs -- so a captured CUDA
+// graph replays with the epoch its previous replay advanced (epoch_add_kernel)
+__device__ __forceinline__ unsigned long long flag_value(unsigned long long value,
+                                                         const long long* epoch) {
+  return epoch ? static_cast<unsigned long long>(*epoch + static_cast<long long>(value)) : value;
+}
+
+__global__ void epoch_add_kernel(long long* epoch, long long delta) { *epoch += delta; }
+
+__global__ void flag_set_kernel(unsigned long long* flag, unsigned long long value,
+                                const long long* epoch) {
+  value = flag_value(value, epoch);
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
@@ -47,7 +59,9 @@ static FlagError* error_block() {
 }
 
 __global__ void flag_wait_kernel(const unsigned long long* flag, unsigned long long value,
-                                 unsigned long long timeout_ns, FlagError* err) {
+                                 unsigned long long timeout_ns, FlagError* err,
+                                 const long long* epoch) {
+  value = flag_value(value, epoch);
   unsigned long long t0;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
   for (;;) {
@@ -69,18 +83,25 @@ __global__ void flag_wait_kernel(const unsigned long long* flag, unsigned long l
   }
 }
 
-int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s) {
-  flag_set_kernel<<<1, 1, 0, s>>>(flag, value);
+int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s,
+                    const long long* epoch) {
+  flag_set_kernel<<<1, 1, 0, s>>>(flag, value, epoch);
   return cuda_status(cudaGetLastError(), "flag_set");
 }
 
 static unsigned long long g_timeout_ns = 30ull * 1000000000ull;
 
-int launch_flag_wait(const unsigned long long* flag, unsigned long long value, cudaStream_t s) {
+int launch_flag_wait(const unsigned long long* flag, unsigned long long value, cudaStream_t s,
+                     const long long* epoch) {
   FlagError* err = error_block();
   if (!err) return cuda_status(g_err_alloc, "cudaHostAlloc(flag error block)");
-  flag_wait_kernel<<<1, 1, 0, s>>>(flag, value, g_timeout_ns, err);
+  flag_wait_kernel<<<1, 1, 0, s>>>(flag, value, g_timeout_ns, err, epoch);
   return cuda_status(cudaGetLastError(), "flag_wait");
+}
+
+int launch_epoch_add(long long* epoch, long long delta, cudaStream_t s) {
+  epoch_add_kernel<<<1, 1, 0, s>>>(epoch, delta);
+  return cuda_status(cudaGetLastError(), "epoch_add");
 }
 
 int poll_flag_error() {

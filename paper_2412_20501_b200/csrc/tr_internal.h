@@ -38,6 +38,9 @@ struct AttnPlan {
   unsigned int* done_count;
   unsigned long long* done_flag;
   unsigned long long done_value;
+  // epoch-relative done value (CUDA-graph replays): when set, the flag is
+  // raised to *done_epoch + (signed) done_value, read when the kernel ends
+  const long long* done_epoch;
   // Longest-first CTA order for multi-segment causal launches (n_order > 0):
   // heads in groups of `head_group` (so a group's K/V stays in L2); inside a
   // group the (segment, tile) classes run in order[] -- sorted by decreasing
@@ -56,8 +59,10 @@ __device__ __forceinline__ void signal_done(const AttnPlan& p) {
   if (prev == gridDim.x - 1) {
     *p.done_count = 0u;
     asm volatile("fence.acq_rel.sys;" ::: "memory");
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.done_flag), "l"(p.done_value)
-                 : "memory");
+    const unsigned long long v =
+        p.done_epoch ? static_cast<unsigned long long>(*p.done_epoch + static_cast<long long>(p.done_value))
+                     : p.done_value;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.done_flag), "l"(v) : "memory");
   }
 }
 
@@ -65,7 +70,11 @@ __device__ __forceinline__ void signal_done(const AttnPlan& p) {
 int launch_attn_sm100(const void* q, const void* k, const void* v, int64_t tq_total,
                       int64_t tk_total, int head_dim, AttnPlan& plan, cudaStream_t s);
 // generic CUDA-core kernel for any head_dim <= 256 (small shapes, odd dims)
-int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s);
+int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s,
+                    const long long* epoch = nullptr);
+int launch_flag_wait(const unsigned long long* flag, unsigned long long value, cudaStream_t s,
+                     const long long* epoch = nullptr);
+int launch_epoch_add(long long* epoch, long long delta, cudaStream_t s);
 // host-mapped record of a timed-out flag wait (p2p_flags.cu)
 int poll_flag_error();
 void clear_flag_error();

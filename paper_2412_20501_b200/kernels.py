@@ -128,7 +128,7 @@ def attention_segments(q, k, v, q_segs, kv_segs, causal, out, lse):
 
 
 def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shift,
-                            done_count=None, done_flag=None, done_value=0):
+                            done_count=None, done_flag=None, done_value=0, epoch=None):
     """``attention_segments`` whose epilogue writes straight into a message
     receive buffer -- typically the home rank's, mapped over CUDA IPC, so the
     OUT_LSE message of the next step (ref engine.py:346-353) travels over
@@ -136,7 +136,10 @@ def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shif
     (H, n) float32 hold q rows [row_shift, row_shift + n).  With
     ``done_flag`` (an int64 device tensor element, possibly a peer's) the
     kernel's last CTA raises it to ``done_value``; ``done_count`` is a zeroed
-    int32 device counter owned by the caller's stream."""
+    int32 device counter owned by the caller's stream.  With ``epoch`` (a
+    one-element int64 device tensor) ``done_value`` is an offset: the flag is
+    raised to ``epoch + done_value`` as the epoch reads when the kernel ends
+    (CUDA-graph replays; tr_attention_segments_push_rel)."""
     _check_qkv(q, k, v)
     _require_cuda("out", out, torch.bfloat16)
     _require_cuda("lse", lse, torch.float32)
@@ -154,11 +157,21 @@ def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shif
         _require_cuda("done_count", done_count, torch.int32)
     qs, ks = _segs(q_segs), _segs(kv_segs)
     with _on(q):
-        _lib.check(_lib.lib().tr_attention_segments_push(
-            _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0], q.shape[1],
-            q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0, row_shift, n,
-            None if done_count is None else _ptr(done_count),
-            None if done_flag is None else _ptr(done_flag), done_value, _stream(q.device)))
+        if epoch is not None:
+            if done_flag is None:
+                raise DimensionError("epoch needs done_flag")
+            _require_cuda("epoch", epoch, torch.int64)
+            _lib.check(_lib.lib().tr_attention_segments_push_rel(
+                _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0],
+                q.shape[1], q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0,
+                row_shift, n, _ptr(done_count), _ptr(done_flag), _ptr(epoch), int(done_value),
+                _stream(q.device)))
+        else:
+            _lib.check(_lib.lib().tr_attention_segments_push(
+                _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), q.shape[0], k.shape[0],
+                q.shape[1], q.shape[2], qs, len(q_segs), ks, len(kv_segs), 1 if causal else 0,
+                row_shift, n, None if done_count is None else _ptr(done_count),
+                None if done_flag is None else _ptr(done_flag), done_value, _stream(q.device)))
     _count(1)
     return out, lse
 
@@ -257,20 +270,42 @@ def splitmix_bf16_(dst, seed, first, low=-1.0, high=1.0):
     return dst
 
 
-def flag_set_(flag, value, stream=None):
+def flag_set_(flag, value, stream=None, epoch=None):
     """Raise a (possibly peer-mapped) int64 sequence flag after all prior work
-    on ``stream`` (system-scope release store)."""
+    on ``stream`` (system-scope release store).  With ``epoch`` (one-element
+    int64 device tensor) the value is ``epoch + value``, read on the device."""
     s = stream or torch.cuda.current_stream(flag.device)
     with torch.cuda.device(s.device):
-        _lib.check(_lib.lib().tr_flag_set(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
+        if epoch is None:
+            _lib.check(_lib.lib().tr_flag_set(_ptr(flag), int(value),
+                                              ctypes.c_void_p(s.cuda_stream)))
+        else:
+            _lib.check(_lib.lib().tr_flag_set_rel(_ptr(flag), _ptr(epoch), int(value),
+                                                  ctypes.c_void_p(s.cuda_stream)))
     _count(1)
 
 
-def flag_wait_(flag, value, stream=None):
-    """Make ``stream`` wait until ``flag >= value`` (one-thread acquire spin)."""
+def flag_wait_(flag, value, stream=None, epoch=None):
+    """Make ``stream`` wait until ``flag >= value`` (one-thread acquire spin);
+    with ``epoch``, until ``flag >= epoch + value``."""
     s = stream or torch.cuda.current_stream(flag.device)
     with torch.cuda.device(s.device):
-        _lib.check(_lib.lib().tr_flag_wait(_ptr(flag), int(value), ctypes.c_void_p(s.cuda_stream)))
+        if epoch is None:
+            _lib.check(_lib.lib().tr_flag_wait(_ptr(flag), int(value),
+                                               ctypes.c_void_p(s.cuda_stream)))
+        else:
+            _lib.check(_lib.lib().tr_flag_wait_rel(_ptr(flag), _ptr(epoch), int(value),
+                                                   ctypes.c_void_p(s.cuda_stream)))
+    _count(1)
+
+
+def epoch_add_(epoch, delta, stream=None):
+    """epoch += delta on the device, in ``stream`` order (the last operation of
+    a captured forward: the next replay's flag values move on by delta)."""
+    s = stream or torch.cuda.current_stream(epoch.device)
+    with torch.cuda.device(s.device):
+        _lib.check(_lib.lib().tr_epoch_add(_ptr(epoch), int(delta),
+                                           ctypes.c_void_p(s.cuda_stream)))
     _count(1)
 
 

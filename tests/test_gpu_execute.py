@@ -89,6 +89,28 @@ def test_ring_runner_single_rank_equals_dense():
     close(res.out, res.lse, ref_o, ref_l, "ring P=1")
 
 
+def test_ring_runner_single_rank_graph_replay():
+    """capture() on one rank: replays of the CUDA graph with the static inputs
+    refilled in place equal eager forwards of the same inputs, bit for bit."""
+    from paper_2412_20501_b200 import rng
+    from paper_2412_20501_b200.ring import TokenRingAttention
+    S, H, D = 4096, 4, 128
+    ins = [rng.attention_inputs(sd, S, H, D) for sd in (5, 6)]
+    eager = TokenRingAttention(S, H, D, causal=True)
+    want = []
+    for t in ins:
+        r = eager(*t)
+        want.append((r.out.clone(), r.lse.clone()))
+    runner = TokenRingAttention(S, H, D, causal=True)
+    static = [t.clone() for t in ins[0]]
+    runner.capture(*static)
+    for i in (1, 0, 1):
+        for d, s_ in zip(static, ins[i]):
+            d.copy_(s_)
+        r = runner(*static)
+        assert torch.equal(r.out, want[i][0]) and torch.equal(r.lse, want[i][1]), i
+
+
 def test_block_attention_api_and_errors():
     import paper_2412_20501_b200 as tr
     q, k, v = splitmix.attention_inputs(42, 4, 2, 3)

@@ -185,3 +185,89 @@ def test_fused_full_size_vs_dense_launch(world):
         assert p.exitcode == 0
     for r, wo, wl in got:
         assert wo <= 2e-2 and wl <= 1e-3, (r, wo, wl)
+
+
+GRAPH_SEEDS = (22, 21, 22)
+
+
+def _worker_graph(rank, world, port, S, H, D, causal, q_out, route, transport, nodes, schedule):
+    """capture() once (after two eager warm-up forwards on seed-21 inputs),
+    then replay the CUDA graph for three calls whose inputs are refilled in
+    place; rank 0 is delayed on the device before every replay so its peers
+    run ahead -- the graph's epoch-relative flag values must keep every call's
+    result its own."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_20501_b200 import rng
+        from paper_2412_20501_b200.ring import TokenRingAttention
+        runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
+                                    transport=transport, route=route, nodes=nodes,
+                                    schedule=schedule)
+        inputs = {sd: rng.local_inputs(sd, runner.part, rank, H, D) for sd in (21, 22)}
+        static = [t.clone() for t in inputs[21]]
+        runner.capture(*static)
+        outs = []
+        for sd in GRAPH_SEEDS:
+            for dst, src in zip(static, inputs[sd]):
+                dst.copy_(src)
+            if rank == 0:
+                torch.cuda._sleep(2_000_000)
+            res = runner(*static)
+            outs.append((res.out.clone(), res.lse.clone()))
+        torch.cuda.synchronize()
+        q_out.put((rank, [(o.double().cpu().numpy(), l.double().cpu().numpy()) for o, l in outs]))
+        runner.close()
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,S,H,D,causal,route,transport", [
+    (2, 2048, 2, 128, True, "ring", "ipc"), (4, 4096, 2, 128, True, "ring", "fused"),
+    (3, 3072, 2, 64, False, "ring", "fused"), (4, 4096, 2, 128, True, "direct", "fused"),
+    (8, 8192, 2, 128, True, "ring", "fused"), (4, 2048, 2, 128, False, "hybrid2", "fused"),
+    (4, 4096, 2, 128, True, "ringattn", "fused"), (2, 2048, 2, 128, False, "ringattn", "ipc")])
+def test_token_ring_graph_replay(world, S, H, D, causal, route, transport):
+    """TokenRingAttention.capture(): CUDA-graph replays on every transport
+    that supports them, checked call by call against the oracle's execute."""
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _port()
+    nodes = int(route[6:]) if route.startswith("hybrid") else 1
+    schedule = "ring" if route == "ringattn" else "token-ring"
+    route = "ring" if nodes > 1 or schedule == "ring" else route
+    procs = [ctx.Process(target=_worker_graph,
+                         args=(r, world, port, S, H, D, causal, q_out, route, transport, nodes,
+                               schedule))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    _reap.extend(procs)
+    res = {}
+    for _ in range(world):
+        r, calls_out = q_out.get(timeout=300)
+        res[r] = calls_out
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    if schedule == "ring":
+        sched = osch.ring(world, S, H, D, causal)
+    elif nodes > 1:
+        sched = osch.hybrid(nodes, world // nodes, S, H, D)
+    else:
+        sched = osch.zigzag_token_ring(world, S, H, D) if causal else osch.token_ring(world, S, H, D)
+    refs = {}
+    for sd in set(GRAPH_SEEDS):
+        q, k, v = (splitmix.to_bf16_f64(x) for x in splitmix.attention_inputs(sd, S, H, D))
+        refs[sd] = osch.execute(sched, q, k, v)
+    for r in range(world):
+        for call, sd in enumerate(GRAPH_SEEDS):
+            out, lse = res[r][call]
+            ref = refs[sd][r]
+            assert np.abs(out - ref[0]).max() <= 2e-2, (r, call)
+            fin = np.isfinite(ref[1])
+            assert np.array_equal(np.isfinite(lse), fin)
+            assert np.abs(lse[fin] - ref[1][fin]).max() <= 1e-3, (r, call)
