@@ -67,10 +67,19 @@ def _declare(lib):
                                                ctypes.POINTER(Segment), i32,
                                                ctypes.POINTER(Segment), i32, i32, i64, i64,
                                                vp, vp, ctypes.c_uint64, vp]
-    lib.tr_attention_segments_push_rel.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32,
-                                                   ctypes.POINTER(Segment), i32,
-                                                   ctypes.POINTER(Segment), i32, i32, i64, i64,
-                                                   vp, vp, vp, i64, vp]
+    try:    # A/B builds older than the epoch-relative ABI lack these four
+        lib.tr_attention_segments_push_rel.argtypes = [vp, vp, vp, vp, vp, i64, i64, i32, i32,
+                                                       ctypes.POINTER(Segment), i32,
+                                                       ctypes.POINTER(Segment), i32, i32, i64,
+                                                       i64, vp, vp, vp, i64, vp]
+        lib.tr_flag_set_rel.argtypes = [vp, vp, i64, vp]
+        lib.tr_flag_wait_rel.argtypes = [vp, vp, i64, vp]
+        lib.tr_epoch_add.argtypes = [vp, i64, vp]
+        for name in ("tr_attention_segments_push_rel", "tr_flag_set_rel", "tr_flag_wait_rel",
+                     "tr_epoch_add"):
+            getattr(lib, name).restype = ctypes.c_int
+    except AttributeError:
+        pass
     lib.tr_merge_state.argtypes = [vp, vp, vp, i32, vp, i64, i32, i32, i64, i64, vp, vp]
     lib.tr_merge_n.argtypes = [vp, vp, i64, ctypes.POINTER(vp), i32, ctypes.POINTER(vp),
                                ctypes.POINTER(i64), i32, i64, i32, i32, vp, vp]
@@ -79,9 +88,6 @@ def _declare(lib):
                                      ctypes.c_double, vp, vp]
     lib.tr_flag_set.argtypes = [vp, ctypes.c_uint64, vp]
     lib.tr_flag_wait.argtypes = [vp, ctypes.c_uint64, vp]
-    lib.tr_flag_set_rel.argtypes = [vp, vp, i64, vp]
-    lib.tr_flag_wait_rel.argtypes = [vp, vp, i64, vp]
-    lib.tr_epoch_add.argtypes = [vp, i64, vp]
     lib.tr_copy_async.argtypes = [vp, vp, ctypes.c_uint64, vp]
     lib.tr_enable_peer_access.argtypes = [i32]
     lib.tr_poll_error.argtypes = []
@@ -90,9 +96,8 @@ def _declare(lib):
     lib.tr_set_flag_timeout_ms.argtypes = [ctypes.c_uint64]
     lib.tr_set_flag_timeout_ms.restype = None
     for name in ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
-                 "tr_attention_segments_push_rel", "tr_merge_state", "tr_merge_n",
+                 "tr_merge_state", "tr_merge_n",
                  "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
-                 "tr_flag_set_rel", "tr_flag_wait_rel", "tr_epoch_add",
                  "tr_copy_async", "tr_enable_peer_access", "tr_poll_error"):
         getattr(lib, name).restype = ctypes.c_int
     lib.tr_version.restype = ctypes.c_char_p
