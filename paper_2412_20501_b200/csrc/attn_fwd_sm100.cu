@@ -122,6 +122,9 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
     }
    } else if (warp == 1 && ntiles > 0) {
     // ------------------------------------------------------------ MMA issuer
+    // one thread, elected once around the loop: plain tcgen05.mma / commit,
+    // descriptors in uniform registers (as the pair kernel, attn_fwd_pair2.cu)
+    if (elect_one_sync()) {
     const uint32_t q_addr = smem_u32(sQ);
     const uint32_t kv_addr = smem_u32(sKV);
     mbar_wait(q_full, 0);
@@ -137,7 +140,7 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const uint32_t off = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
-        mma_ss_elect(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
+        mma_ss(tmem + h * 128, desc_add(a0, off), desc_add(b0, off), C::IDESC_QK, kk > 0);
       }
     };
     // O_h += P_h[:, keys of chunk kh] . V[keys of chunk kh, :]
@@ -152,10 +155,10 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
         // experiment: A (P) from shared memory, SS mode
         const uint64_t a0 = dQ + static_cast<uint32_t>((h * C::TILE) >> 4);
         const uint32_t offa = ((kk / 4) * C::BOX + (kk % 4) * 32) >> 4;
-        mma_ss_elect(tmem + 256 + h * 128, desc_add(a0, offa), desc_add(b0, (kk * 2048) >> 4),
+        mma_ss(tmem + 256 + h * 128, desc_add(a0, offa), desc_add(b0, (kk * 2048) >> 4),
                      C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
 #else
-        mma_ts_elect(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
+        mma_ts(tmem + 256 + h * 128, tmem + h * 128 + kk * 8, desc_add(b0, (kk * 2048) >> 4),
                      C::IDESC_PV, (acc || kk > 0) ? 1u : 0u);
 #endif
       }
@@ -179,27 +182,29 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
       TR_TRACE_AT(0, j);
       qk(0, sk);
       TR_TRACE_AT(1, j);
-      tc_commit_elect(&s_full[0]);
+      tc_commit(&s_full[0]);
       if (j > 0) {
         pv_both(1, prev_v_stage, (j - 1) & 1, j - 1 > 0);
-        tc_commit_elect(&kv_empty[prev_v_stage]);
+        tc_commit(&kv_empty[prev_v_stage]);
       }
       TR_TRACE_AT(2, j);
       qk(1, sk);
-      tc_commit_elect(&s_full[1]);
-      tc_commit_elect(&kv_empty[sk]);
+      tc_commit(&s_full[1]);
+      tc_commit(&kv_empty[sk]);
       mbar_wait(&kv_full[sv], rv & 1);
       TR_TRACE_AT(3, j);
       pv_both(0, sv, j & 1, j > 0);
       TR_TRACE_AT(4, j);
-      if (j == ntiles - 1) tc_commit_elect(&o_done[0]);
+      if (j == ntiles - 1) tc_commit(&o_done[0]);
       prev_v_stage = sv;
       sk = (sv + 1 == C::NS) ? 0 : sv + 1;
       rk = (sv + 1 == C::NS) ? rv + 1 : rv;
     }
     pv_both(1, prev_v_stage, (ntiles - 1) & 1, ntiles - 1 > 0);
-    tc_commit_elect(&kv_empty[prev_v_stage]);
-    tc_commit_elect(&o_done[1]);
+    tc_commit(&kv_empty[prev_v_stage]);
+    tc_commit(&o_done[1]);
+    }
+    __syncwarp();
    }
   } else {
    setmaxnreg_inc<224>();
