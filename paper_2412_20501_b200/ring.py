@@ -158,6 +158,15 @@ def compile_rank(sched, rank: int) -> list:
     return prog
 
 
+def _nvtx_push(name):
+    # NVTX ranges per TokenRing step (host side; visible in nsys / ncu --nvtx)
+    torch.cuda.nvtx.range_push(name)
+
+
+def _nvtx_pop():
+    torch.cuda.nvtx.range_pop()
+
+
 def _ptrs(*ts):
     return tuple(t.data_ptr() for t in ts)
 
@@ -477,6 +486,7 @@ class TokenRingAttention:
         for st in self.prog:
             i = st.step
             ev = {}
+            _nvtx_push(f"tokenring step {i}")
             if self.record_timeline:
                 ev["start"] = self.ops.event()
                 self.ops.record(ev["start"])
@@ -595,6 +605,7 @@ class TokenRingAttention:
             # this step's compute and my own forward copies are done
             cs.wait_event(ev_comp[i])
             kernels.flag_set_(self.flags[1:2], i, cs, epoch=E)
+            _nvtx_pop()
         last = self.prog[-1]
         if fused:
             self._merge_all_fused(cur, local_layout)
@@ -709,6 +720,7 @@ class TokenRingAttention:
         for st in self.prog:
             i = st.step
             ev = {}
+            _nvtx_push(f"tokenring step {i}")
             if self.record_timeline:
                 ev["start"] = self.ops.event()
                 self.ops.record(ev["start"])
@@ -786,6 +798,7 @@ class TokenRingAttention:
                 ev["computed"] = self.ops.event()
                 self.ops.record(ev["computed"])
                 self.timeline.append(ev)
+            _nvtx_pop()
         for r in pending:
             r.wait()
         if pending_out:
