@@ -31,7 +31,8 @@ buf = np.zeros(2 * 20 * 64 * 8, dtype=np.uint64)
 L = _lib.lib()
 L.tr_debug_trace_pair2.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert L.tr_debug_trace_pair2(buf.ctypes.data, buf.nbytes) == 0
-t = buf.reshape(2, 20, 64, 8).astype(np.int64)[0]      # CTA 0
+t_all = buf.reshape(2, 20, 64, 8).astype(np.int64)
+t = t_all[0]                                           # CTA 0
 J = np.arange(8, 56)
 mma = t[1]
 med = lambda x: float(np.median(x))  # noqa: E731
@@ -84,3 +85,14 @@ for w in (4, 5, 8, 9):
             (f"w{w} next S ready", t[w][j0 + 1, 1])]
 for name, x in sorted(evs, key=lambda e: e[1]):
     print(f"  {int(x - base):7d}  {name}")
+
+# CTA 1 (the follower; its own SM clock): S ready -> P chunks published per half
+t1 = t_all[1]
+if t1[4:12, J, 1].min() > 0:
+    for half, ws in ((0, range(4, 8)), (1, range(8, 12))):
+        sw = t1[list(ws)]
+        print(f"CTA 1 half {half}: S ready -> max {med(sw[:, J, 2].max(0) - sw[:, J, 1].min(0)):.0f} -> "
+              f"c0 pub {med(sw[:, J, 3].max(0) - sw[:, J, 2].max(0)):.0f} -> c1 pub "
+              f"{med(sw[:, J, 4].max(0) - sw[:, J, 3].max(0)):.0f} | S ready -> c1 pub "
+              f"{med(sw[:, J, 4].max(0) - sw[:, J, 1].min(0)):.0f} (CTA 0: "
+              f"{med(t[list(ws)][:, J, 4].max(0) - t[list(ws)][:, J, 1].min(0)):.0f})")
