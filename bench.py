@@ -218,6 +218,12 @@ def _exec_sample_worker(args):
             return flops * n, busy, n
 
 
+def host_info():
+    """The host facts SURVEY 8(d) asks the CPU baseline to report."""
+    return {"os_cpu_count": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0)),
+            "openblas_num_threads_per_process": 1}
+
+
 def cpu_exec_rate(schedule, causal, D, budget_s=8.0, workers=None):
     """Aggregate CPU TFLOP/s of the reference's CPU path on this host: every
     core runs the reference's own ``execute`` of the benchmarked schedule
@@ -284,7 +290,8 @@ def run_reference(a):
         "tokens_per_s": S / sec_per_step,
         "cpu_baseline": {"value": tflops, "unit": "TFLOP/s", "cores": r0["workers"],
                          "kind": r0["kind"], "path": "engine.execute (numpy backend)",
-                         "extrapolated": True, "sample": _exec_sample_text(r0, a)},
+                         "extrapolated": True, "sample": _exec_sample_text(r0, a),
+                         "host": host_info()},
         "cpu_baseline_cython": cy,
         "e2e": {"value": tflops, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -717,7 +724,7 @@ def run_ours(a):
             line["cpu_baseline"] = {
                 "value": r["tflops"], "unit": "TFLOP/s", "cores": r["workers"], "kind": r["kind"],
                 "path": "engine.execute (numpy backend)", "extrapolated": True,
-                "sample": _exec_sample_text(r, a)}
+                "sample": _exec_sample_text(r, a), "host": host_info()}
         print(json.dumps(line), flush=True)
     if world > 1:
         for r in runners:
