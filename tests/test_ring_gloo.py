@@ -169,3 +169,37 @@ def test_ring_attention_gloo(world, S, causal):
                                  [res[r][1] for r in range(world)], osch.ranges_of(sched, S), S)
     d_out, d_lse = ok.dense_attention(q, k, v, causal)
     assert ok.max_relative_error(g_out, g_lse, d_out, d_lse) <= 2e-2
+
+
+def _worker_capture(rank, world, port, result_q):
+    """capture() refuses the NCCL transport (P2P ops of a process group are
+    not captured); checked before any device work."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from cpu_ops import OracleOps
+        from paper_2412_20501_b200.errors import ConfigError
+        from paper_2412_20501_b200.ring import TokenRingAttention
+        runner = TokenRingAttention(64, 2, 8, causal=True, ops=OracleOps(), device="cpu")
+        try:
+            runner.capture(None, None, None)
+            result_q.put((rank, "no error"))
+        except ConfigError as e:
+            result_q.put((rank, "ConfigError" if "ipc or fused" in str(e) else str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_capture_refuses_nccl_transport():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_capture, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    _reap.extend(procs)
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    assert got == {0: "ConfigError", 1: "ConfigError"}, got
