@@ -191,6 +191,35 @@ def test_flag_wait_timeout_is_a_schedule_error(K):
         K.clear_error()
 
 
+def test_epoch_relative_flags(K):
+    """tr_flag_set_rel / tr_flag_wait_rel / tr_epoch_add: values are
+    epoch + offset read on the device when the operation runs, so the same
+    enqueued (or captured) sequence moves on with the epoch."""
+    flag = torch.zeros(1, dtype=torch.int64, device="cuda")
+    epoch = torch.full((1,), 100, dtype=torch.int64, device="cuda")
+    K.clear_error()
+    K.set_flag_timeout_ms(200)
+    try:
+        K.flag_set_(flag, 3, epoch=epoch)                    # flag = 103
+        K.flag_wait_(flag, 3, epoch=epoch)                   # 103 >= 103: passes
+        torch.cuda.synchronize()
+        K.poll_error()
+        assert int(flag.item()) == 103
+        K.epoch_add_(epoch, 10)                              # epoch = 110
+        K.flag_wait_(flag, 3, epoch=epoch)                   # 103 < 113: times out
+        torch.cuda.synchronize()
+        from paper_2412_20501_b200.errors import ScheduleError
+        with pytest.raises(ScheduleError, match="not delivered"):
+            K.poll_error()
+        K.clear_error()
+        K.flag_set_(flag, -2, epoch=epoch)                   # negative offset: 108
+        torch.cuda.synchronize()
+        assert int(flag.item()) == 108 and int(epoch.item()) == 110
+    finally:
+        K.set_flag_timeout_ms(30000)
+        K.clear_error()
+
+
 def test_segments_zigzag_step0(K):
     """Zigzag step 0 of rank r: q{lo,hi} x kv{lo,hi} by global positions."""
     P, c, h, d = 4, 256, 2, 128
