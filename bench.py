@@ -373,47 +373,75 @@ def ncu_traffic():
         return None
 
 
-def e2e_pipelined(make_runner, q, k, v, steps, barrier, allmax, groups):
+def e2e_pipelined(make_runner, q, k, v, steps, barrier, allmax, groups, edge=0,
+                  return_outputs=False):
     """End to end through the public API with host buffers.  Heads are
-    independent, so the inputs live on the host as `groups` head groups
-    (contiguous (T, H/groups, D) pinned buffers) and every step runs one
-    TokenRing forward per group (a TokenRingAttention over H/groups heads):
-    H2D of the next group's q/k/v and D2H of the previous group's bf16 output
-    and lse overlap the current group's compute on their own streams, so only
-    one group's input copy (pipeline fill) and one group's output copy
-    (drain) are exposed per timed run.  Every step's copies are inside the
-    timed region.  Returns ms per step (max over ranks)."""
+    independent, so the inputs live on the host as head groups (contiguous
+    (T, heads, D) pinned buffers) and every step runs one TokenRing forward
+    per group (a TokenRingAttention over that many heads): H2D of the next
+    group's q/k/v and D2H of the previous group's bf16 output and lse overlap
+    the current group's compute on their own streams, so only the first
+    group's input copy (pipeline fill) and the last group's output copy
+    (drain) are exposed per timed run -- and with ``edge`` > 0 the run's very
+    first and very last groups are split so that those two are only ``edge``
+    heads each.  Every step's copies are inside the timed region.  Returns ms
+    per step (max over ranks); with ``return_outputs`` also the pinned host
+    outputs, {(h0, h1): [[out, lse] for the two step parities]}."""
     import torch
-    H = q.shape[1]
+    T, H, D = q.shape
     G = groups
     hg = H // G
-    runner = make_runner(hg)
+    edge = edge if 0 < edge < hg else 0
+    runners = {}
+
+    def runner_for(n):
+        if n not in runners:
+            runners[n] = make_runner(n)
+        return runners[n]
+
     cur = torch.cuda.current_stream()
     cs_in, cs_out = torch.cuda.Stream(), torch.cuda.Stream()
-    host_in = [[t[:, g * hg:(g + 1) * hg].contiguous().cpu().pin_memory() for t in (q, k, v)]
-               for g in range(G)]
-    shape = host_in[0][0].shape
-    dev_in = [[torch.empty(shape, dtype=torch.bfloat16, device="cuda") for _ in range(3)]
-              for _ in range(2)]
-    obf = [torch.empty(runner.acc_out.shape, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
-    lsd = [torch.empty_like(runner.acc_lse) for _ in range(2)]
-    oh = [[torch.empty(obf[0].shape, dtype=torch.bfloat16).pin_memory() for _ in range(G)]
-          for _ in range(2)]
-    lh = [[torch.empty(lsd[0].shape, dtype=torch.float32).pin_memory() for _ in range(G)]
-          for _ in range(2)]
+    host_in, host_out = {}, {}
+
+    def host_bufs(h0, h1):
+        if (h0, h1) not in host_in:
+            host_in[(h0, h1)] = [t[:, h0:h1].contiguous().cpu().pin_memory() for t in (q, k, v)]
+            host_out[(h0, h1)] = [
+                [torch.zeros((T, h1 - h0, D), dtype=torch.bfloat16).pin_memory(),
+                 torch.zeros((h1 - h0, T), dtype=torch.float32).pin_memory()] for _ in range(2)]
+        return host_in[(h0, h1)], host_out[(h0, h1)]
+
+    # device staging: two slots of flat buffers sized for the largest group,
+    # viewed as (T, n, D) for an n-head group
+    dev_flat = [[torch.empty(T * hg * D, dtype=torch.bfloat16, device="cuda") for _ in range(3)]
+                for _ in range(2)]
+    obf_flat = [torch.empty(T * hg * D, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    lsd_flat = [torch.empty(hg * T, dtype=torch.float32, device="cuda") for _ in range(2)]
     ev = {n: [torch.cuda.Event() for _ in range(2)] for n in ("in", "used", "out", "d2h")}
 
+    def pieces(st, g, n):
+        h0, h1 = g * hg, (g + 1) * hg
+        cuts = [h0, h1]
+        if edge and st == 0 and g == 0:
+            cuts.insert(1, h0 + edge)
+        if edge and st == n - 1 and g == G - 1:
+            cuts.insert(len(cuts) - 1, h1 - edge)
+        return [(st, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+
     def run(n):
-        units = [(st, g) for st in range(n) for g in range(G)]
+        units = [u for st in range(n) for g in range(G) for u in pieces(st, g, n)]
+        for _, a, b in units:
+            host_bufs(a, b)
+            runner_for(b - a)
 
         def h2d(u):
             sl = u % 2
-            _, g = units[u]
+            _, a, b = units[u]
             with torch.cuda.stream(cs_in):
                 if u >= 2:
                     cs_in.wait_event(ev["used"][sl])
-                for d, hsrc in zip(dev_in[sl], host_in[g]):
-                    d.copy_(hsrc, non_blocking=True)
+                for d, hsrc in zip(dev_flat[sl], host_in[(a, b)]):
+                    d[:hsrc.numel()].view(hsrc.shape).copy_(hsrc, non_blocking=True)
                 ev["in"][sl].record(cs_in)
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
@@ -421,22 +449,26 @@ def e2e_pipelined(make_runner, q, k, v, steps, barrier, allmax, groups):
         cs_in.wait_stream(cur)
         cs_out.wait_stream(cur)
         h2d(0)
-        for u, (st, g) in enumerate(units):
+        for u, (st, a, b) in enumerate(units):
             sl = u % 2
+            nh = b - a
             if u + 1 < len(units):
                 h2d(u + 1)
             cur.wait_event(ev["in"][sl])
-            res = runner(*dev_in[sl])
+            res = runner_for(nh)(*[d[:T * nh * D].view(T, nh, D) for d in dev_flat[sl]])
             ev["used"][sl].record(cur)
             if u >= 2:
                 cur.wait_event(ev["d2h"][sl])
-            obf[sl].copy_(res.out)
-            lsd[sl].copy_(res.lse)
+            obf = obf_flat[sl][:T * nh * D].view(T, nh, D)
+            lsd = lsd_flat[sl][:nh * T].view(nh, T)
+            obf.copy_(res.out)                  # bf16 output, the inputs' dtype
+            lsd.copy_(res.lse)
             ev["out"][sl].record(cur)
             with torch.cuda.stream(cs_out):
                 cs_out.wait_event(ev["out"][sl])
-                oh[st % 2][g].copy_(obf[sl], non_blocking=True)
-                lh[st % 2][g].copy_(lsd[sl], non_blocking=True)
+                oh, lh = host_out[(a, b)][st % 2]
+                oh.copy_(obf, non_blocking=True)
+                lh.copy_(lsd, non_blocking=True)
                 ev["d2h"][sl].record(cs_out)
         cur.wait_stream(cs_out)
         end.record(cur)
@@ -448,7 +480,8 @@ def e2e_pipelined(make_runner, q, k, v, steps, barrier, allmax, groups):
     s, e = run(steps)
     torch.cuda.synchronize()
     barrier()
-    return allmax([s.elapsed_time(e) / steps])[0]
+    ms = allmax([s.elapsed_time(e) / steps])[0]
+    return (ms, host_out) if return_outputs else ms
 
 
 def exchange_report(world, runner, xsum, n_fwd, shared):
@@ -675,17 +708,21 @@ def run_ours(a):
             runners.append(TokenRingAttention(S, hg, D, causal=causal, transport=transport,
                                               schedule=a.schedule))
             return runners[-1]
-        e2e_ms = e2e_pipelined(make_runner, q, k, v, e2e_steps, barrier, allmax, groups)
+        # the run's first and last groups split off a quarter-size piece, so the
+        # exposed pipeline fill / drain is a quarter of a group's copy
+        edge = (H // groups) // 4
+        e2e_ms = e2e_pipelined(make_runner, q, k, v, e2e_steps, barrier, allmax, groups, edge)
         h2d = 3 * q.numel() * 2 * world
         d2h = (q.numel() * 2 + runner.acc_lse.numel() * 4) * world
         e2e = {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-               "steps": e2e_steps, "head_groups": groups,
+               "steps": e2e_steps, "head_groups": groups, "edge_heads": edge,
                "api": "TokenRingAttention.__call__ -> tr_attention_segments(_push) / tr_merge_n "
                       "(C ABI), one call per head group of H/head_groups heads; each step's "
                       "q/k/v copied in from pinned host memory and its bf16 output + lse "
                       "copied out, group by group, on copy streams double-buffered against "
-                      "the neighbouring groups' compute"}
+                      "the neighbouring groups' compute (the run's first and last groups split "
+                      "off edge_heads-head pieces to shorten the exposed fill and drain)"}
 
     if rank == 0:
         peaks, peak_src = measured_peaks()

@@ -111,6 +111,31 @@ def test_ring_runner_single_rank_graph_replay():
         assert torch.equal(r.out, want[i][0]) and torch.equal(r.lse, want[i][1]), i
 
 
+def test_bench_e2e_pipeline_outputs():
+    """bench.py's end-to-end leg (head groups, edge pieces, copy streams,
+    double-buffered staging) hands back in pinned host memory exactly what
+    one runner over all heads computes on the device."""
+    import bench
+    from paper_2412_20501_b200 import rng
+    from paper_2412_20501_b200.ring import TokenRingAttention
+    S, H, D = 4096, 8, 128
+    q, k, v = rng.attention_inputs(11, S, H, D)
+    ref = TokenRingAttention(S, H, D, causal=True)(q, k, v)
+    want_o, want_l = ref.out.to(torch.bfloat16).cpu(), ref.lse.cpu()
+    ms, outs = bench.e2e_pipelined(lambda n: TokenRingAttention(S, n, D, causal=True),
+                                   q, k, v, 3, lambda: None, lambda x: x, 2, edge=1,
+                                   return_outputs=True)
+    assert ms > 0
+    # groups of 4 heads; the run's first and last groups split off 1-head pieces
+    assert set(outs) == {(0, 4), (4, 8), (0, 1), (1, 4), (4, 7), (7, 8)}
+    for (a, b), slots in outs.items():
+        for o, l in slots:
+            if not l.abs().sum():          # a parity this range never ran at
+                continue
+            assert torch.equal(o, want_o[:, a:b]), (a, b)
+            assert torch.equal(l, want_l[a:b]), (a, b)
+
+
 def test_block_attention_api_and_errors():
     import paper_2412_20501_b200 as tr
     q, k, v = splitmix.attention_inputs(42, 4, 2, 3)
