@@ -496,7 +496,8 @@ def group_computes(sched: Schedule, computes) -> tuple | None:
 
 
 # ----------------------------------------------------------------- executor
-def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list | None = None):
+def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list | None = None,
+            check_finite: bool = True):
     """Run a schedule with all simulated ranks on the current GPU.
 
     Same contract as ``ringsim.engine.execute`` (ref engine.py:468-638):
@@ -507,10 +508,13 @@ def execute(sched: Schedule, q, k, v, causal: bool | None = None, timeline: list
     If ``timeline`` is a list, (step, rank, start_event, end_event) CUDA
     event pairs bracketing every rank's attention launch are appended to it
     (the measured counterpart of the reference's netsim compute lane).
+    ``check_finite=False`` skips the non-finite input check (ref core.py:96-104),
+    a device-to-host read that blocks the host until the GPU is idle -- for
+    timing loops that checked their inputs once beforehand.
     """
     if causal is not None and causal != sched.causal:
         raise ConfigError(f"schedule was built causal={sched.causal}, got causal={causal}")
-    q, k, v = check_qkv(q, k, v)
+    q, k, v = check_qkv(q, k, v, check_finite)
     shape = (sched.partition.seq_len, sched.heads, sched.head_dim)
     if tuple(q.shape) != shape:
         raise DimensionError(f"q must have shape {shape}, got {tuple(q.shape)}")
