@@ -109,6 +109,19 @@ int tr_attention_segments_push_rel(const void* q, const void* k, const void* v, 
                                    uint64_t* done_flag, const int64_t* done_epoch,
                                    int64_t done_offset, void* stream);
 
+/* Launch option of the calling thread's later D=128 attention launches
+ * (tr_attention_block / _segments / _segments_push*): when on, each is a
+ * programmatic dependent launch of the previous kernel on its stream, so its
+ * CTAs start on the SMs the previous grid's last wave frees instead of after
+ * the whole grid (the attention kernel triggers its dependents as soon as all
+ * of its CTAs are resident).  The launch does not wait for the previous
+ * kernel's results: only for a TokenRing step whose inputs were complete
+ * before that kernel (every message it reads was waited for by an earlier
+ * kernel).  Returns the previous setting; off by default.  No counterpart in
+ * the reference, whose steps run one after another on the host
+ * (engine.py:468-638). */
+int32_t tr_set_launch_overlap(int32_t on);
+
 /* kernels.merge_state, in place on a float32 accumulator:
  *   acc <- merge(acc, blk)     (ref _kernels.pyx:68-102)
  * blk_out is bf16 or f32 (blk_dtype); -inf rows are exact identities.

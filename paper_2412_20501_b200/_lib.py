@@ -36,7 +36,7 @@ EXPORTS = ("tr_attention_block", "tr_attention_segments", "tr_attention_segments
            "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait", "tr_flag_set_rel",
            "tr_flag_wait_rel", "tr_epoch_add", "tr_copy_async",
            "tr_enable_peer_access", "tr_poll_error", "tr_clear_error",
-           "tr_set_flag_timeout_ms", "tr_version",
+           "tr_set_flag_timeout_ms", "tr_set_launch_overlap", "tr_version",
            "tr_kernel_count", "tr_kernel_name", "tr_last_error")
 
 
@@ -95,6 +95,9 @@ def _declare(lib):
     lib.tr_clear_error.restype = None
     lib.tr_set_flag_timeout_ms.argtypes = [ctypes.c_uint64]
     lib.tr_set_flag_timeout_ms.restype = None
+    if hasattr(lib, "tr_set_launch_overlap"):   # absent from older A/B builds
+        lib.tr_set_launch_overlap.argtypes = [i32]
+        lib.tr_set_launch_overlap.restype = i32
     for name in ("tr_attention_block", "tr_attention_segments", "tr_attention_segments_push",
                  "tr_merge_state", "tr_merge_n",
                  "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",

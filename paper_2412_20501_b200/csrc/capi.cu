@@ -16,8 +16,10 @@
 namespace tr {
 
 static thread_local std::string g_last_error;
+static thread_local int32_t g_launch_overlap = 0;   // tr_set_launch_overlap
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+bool launch_overlap() { return g_launch_overlap != 0; }
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -159,6 +161,7 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   plan.done_flag = push.done_flag;
   plan.done_value = push.done_value;
   plan.done_epoch = push.done_epoch;
+  plan.overlap_prev = launch_overlap() ? 1 : 0;
   plan.tile_prefix[0] = 0;
   for (int i = 0; i < plan.nq; ++i)
     plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
@@ -360,6 +363,12 @@ int tr_enable_peer_access(int32_t peer_device) {
 }
 
 int tr_poll_error(void) { return poll_flag_error(); }
+
+int32_t tr_set_launch_overlap(int32_t on) {
+  const int32_t prev = g_launch_overlap;
+  g_launch_overlap = on ? 1 : 0;
+  return prev;
+}
 void tr_clear_error(void) { clear_flag_error(); }
 void tr_set_flag_timeout_ms(uint64_t ms) { set_flag_timeout_ns(ms * 1000000ull); }
 

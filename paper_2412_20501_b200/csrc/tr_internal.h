@@ -48,6 +48,9 @@ struct AttnPlan {
   // plain order (head-major, each causal segment heaviest tile first).
   int32_t n_order;
   int32_t head_group;
+  // host side: launch as a programmatic dependent of the previous kernel on
+  // the stream (tr_set_launch_overlap); the kernel itself never waits on it
+  int32_t overlap_prev;
   uint16_t order[TR_ORDER_MAX];
 };
 
@@ -79,6 +82,8 @@ int launch_epoch_add(long long* epoch, long long delta, cudaStream_t s);
 int poll_flag_error();
 void clear_flag_error();
 void set_flag_timeout_ns(unsigned long long ns);
+// thread-local launch option of the tcgen05 attention launches (tr_set_launch_overlap)
+bool launch_overlap();
 int launch_attn_simt(const void* q, const void* k, const void* v, int head_dim, AttnPlan& plan,
                      cudaStream_t s);
 bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const void* v,

@@ -176,6 +176,26 @@ def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shif
     return out, lse
 
 
+class overlap_launches:
+    """Context manager: the D=128 attention launches made inside it (this
+    thread) are programmatic dependent launches of the previous kernel on
+    their stream -- their CTAs take the SMs the previous grid's last wave
+    frees instead of waiting for the whole grid (tr_set_launch_overlap).
+    Only for launches that read nothing the previous kernel writes, e.g.
+    TokenRing steps whose messages were waited for by an earlier kernel."""
+
+    def __init__(self, on=True):
+        self.on = bool(on)
+
+    def __enter__(self):
+        self.prev = _lib.lib().tr_set_launch_overlap(1 if self.on else 0)
+        return self
+
+    def __exit__(self, *exc):
+        _lib.lib().tr_set_launch_overlap(self.prev)
+        return False
+
+
 def merge_state_(acc_out, acc_lse, blk_out, blk_lse, final_out=None):
     """In place: acc <- merge(acc, blk).  acc_out float32 (T,H,D); acc_lse /
     blk_lse may be column slices of wider (H, S) buffers (row stride S)."""

@@ -36,7 +36,8 @@ def test_header_declares_expected_api():
                           "tr_partial_init", "tr_splitmix_bf16", "tr_flag_set", "tr_flag_wait",
                           "tr_flag_set_rel", "tr_flag_wait_rel", "tr_epoch_add",
                           "tr_copy_async", "tr_enable_peer_access", "tr_poll_error",
-                          "tr_clear_error", "tr_set_flag_timeout_ms", "tr_version",
+                          "tr_clear_error", "tr_set_flag_timeout_ms", "tr_set_launch_overlap",
+                          "tr_version",
                           "tr_kernel_count", "tr_kernel_name", "tr_last_error"])
 
 
