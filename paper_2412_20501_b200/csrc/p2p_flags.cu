@@ -85,8 +85,9 @@ __global__ void flag_wait_kernel(const unsigned long long* flag, unsigned long l
 
 int launch_flag_set(unsigned long long* flag, unsigned long long value, cudaStream_t s,
                     const long long* epoch) {
-  flag_set_kernel<<<1, 1, 0, s>>>(flag, value, epoch);
-  return cuda_status(cudaGetLastError(), "flag_set");
+  return cuda_status(launch_kernel(flag_set_kernel, dim3(1), dim3(1), 0, s, launch_overlap(), flag,
+                                   value, epoch),
+                     "flag_set");
 }
 
 static unsigned long long g_timeout_ns = 30ull * 1000000000ull;
@@ -95,8 +96,11 @@ int launch_flag_wait(const unsigned long long* flag, unsigned long long value, c
                      const long long* epoch) {
   FlagError* err = error_block();
   if (!err) return cuda_status(g_err_alloc, "cudaHostAlloc(flag error block)");
-  flag_wait_kernel<<<1, 1, 0, s>>>(flag, value, g_timeout_ns, err, epoch);
-  return cuda_status(cudaGetLastError(), "flag_wait");
+  // (overlap: the wait may start while the previous kernel still runs; its
+  // dependents start only once it has returned -- it never triggers early)
+  return cuda_status(launch_kernel(flag_wait_kernel, dim3(1), dim3(1), 0, s, launch_overlap(),
+                                   flag, value, g_timeout_ns, err, epoch),
+                     "flag_wait");
 }
 
 int launch_epoch_add(long long* epoch, long long delta, cudaStream_t s) {

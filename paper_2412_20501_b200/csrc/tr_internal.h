@@ -82,8 +82,32 @@ int launch_epoch_add(long long* epoch, long long delta, cudaStream_t s);
 int poll_flag_error();
 void clear_flag_error();
 void set_flag_timeout_ns(unsigned long long ns);
-// thread-local launch option of the tcgen05 attention launches (tr_set_launch_overlap)
+// thread-local launch option (tr_set_launch_overlap): attention, flag-wait
+// and flag-set launches become programmatic dependents of the previous
+// kernel on their stream
 bool launch_overlap();
+
+// kernel<<<grid, block, smem, s>>>(args...), or the same as a programmatic
+// dependent launch when `overlap` (cudaLaunchAttributeProgrammaticStreamSerialization)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t s, bool overlap, Args... args) {
+  if (!overlap) {
+    kernel<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 int launch_attn_simt(const void* q, const void* k, const void* v, int head_dim, AttnPlan& plan,
                      cudaStream_t s);
 bool sm100_supports(int head_dim, int heads, const void* q, const void* k, const void* v,

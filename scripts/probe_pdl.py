@@ -45,10 +45,18 @@ def rank_steps(sched, r):
     return steps
 
 
-def run_chain(q, k, v, steps, outs, causal, overlap):
+MODES = ("plain", "overlap", "overlap+event", "overlap+flagwait", "overlap+event+flagwait")
+
+
+def run_chain(q, k, v, steps, outs, causal, mode, flag):
+    overlap = mode != "plain"
     for i, (qs, ks, _) in enumerate(steps):
         o, l = outs[i]
         with kernels.overlap_launches(overlap and i > 0):
+            if i > 0 and "event" in mode:        # what the runner records between steps
+                torch.cuda.Event().record()
+            if i > 0 and "flagwait" in mode:     # an already satisfied message wait
+                kernels.flag_wait_(flag, 1)
             kernels.attention_segments(q, k, v, qs, ks, causal, o, l)
 
 
@@ -60,37 +68,38 @@ def main():
         for S in seqs:
             sched = build(P, S, H, D)
             q, k, v = rng.attention_inputs(0, S, H, D)
-            res = {False: [], True: []}
+            res = {m: [] for m in MODES}
+            flag = torch.ones(1, dtype=torch.int64, device=q.device)
             same = True
             flops_max = 0
             for r in range(P):
                 steps = rank_steps(sched, r)
                 flops_max = max(flops_max, sum(f for _, _, f in steps))
                 outs = {m: [(torch.empty_like(q), torch.empty((H, S), device=q.device))
-                             for _ in steps] for m in (False, True)}
-                times = {False: [], True: []}
+                             for _ in steps] for m in ("plain", "overlap")}
+                times = {m: [] for m in MODES}
                 for it in range(reps + 1):
-                    for m in (False, True):
+                    for m in MODES:
                         torch.cuda.synchronize()
                         e0 = torch.cuda.Event(enable_timing=True)
                         e1 = torch.cuda.Event(enable_timing=True)
                         e0.record()
-                        run_chain(q, k, v, steps, outs[m], causal, m)
+                        run_chain(q, k, v, steps, outs["plain" if m == "plain" else "overlap"],
+                                  causal, m, flag)
                         e1.record()
                         torch.cuda.synchronize()
                         if it > 0:
                             times[m].append(e0.elapsed_time(e1))
-                for (qs, _, _), (oa, la), (ob, lb) in zip(steps, outs[False], outs[True]):
+                for (qs, _, _), (oa, la), (ob, lb) in zip(steps, outs["plain"], outs["overlap"]):
                     for r0, n, _ in qs:
                         same &= torch.equal(oa[r0:r0 + n], ob[r0:r0 + n])
                         same &= torch.equal(la[:, r0:r0 + n], lb[:, r0:r0 + n])
-                for m in (False, True):
+                for m in MODES:
                     res[m].append(statistics.median(times[m]))
-            a, b = max(res[False]), max(res[True])
-            kind = sched.kind
-            print(f"{kind:18s} S={S:7d} P={P}: slowest rank chain plain {a:8.3f} ms "
-                  f"({flops_max / a / 1e9:6.0f} TF)  overlap {b:8.3f} ms "
-                  f"({flops_max / b / 1e9:6.0f} TF)  gain {100 * (a / b - 1):+5.1f} %  "
+            a = max(res["plain"])
+            cols = "  ".join(f"{m} {max(res[m]):.3f} ms ({flops_max / max(res[m]) / 1e9:.0f} TF, "
+                             f"{100 * (a / max(res[m]) - 1):+.1f} %)" for m in MODES)
+            print(f"{sched.kind:18s} S={S:7d} P={P}: slowest rank chain: {cols}  "
                   f"bit-identical {same}")
             sys.stdout.flush()
             del q, k, v

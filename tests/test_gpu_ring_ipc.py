@@ -47,7 +47,7 @@ SEEDS = (21, 22, 21)
 
 
 def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, nodes=1,
-            schedule="token-ring"):
+            schedule="token-ring", overlap_steps=True):
     """Back-to-back calls with different inputs and no host synchronisation
     in between (the runner's flags carry each call's initial conditions);
     rank 0 is delayed on the device before every call so its peers run ahead
@@ -61,7 +61,7 @@ def _worker(rank, world, port, S, H, D, causal, calls, q_out, route, transport, 
         from paper_2412_20501_b200.ring import TokenRingAttention
         runner = TokenRingAttention(S, H, D, causal=causal, device=torch.device("cuda", 0),
                                     transport=transport, route=route, nodes=nodes,
-                                    schedule=schedule)
+                                    schedule=schedule, overlap_steps=overlap_steps)
         inputs = {sd: rng.local_inputs(sd, runner.part, rank, H, D) for sd in set(SEEDS)}
         outs = []
         for sd in SEEDS[:calls]:
@@ -130,6 +130,45 @@ def test_token_ring_ipc(world, S, H, D, causal, route, transport):
             fin = np.isfinite(ref[1])
             assert np.array_equal(np.isfinite(lse), fin)
             assert np.abs(lse[fin] - ref[1][fin]).max() <= 1e-3, (r, call)
+
+
+def _run_workers(world, S, H, D, causal, route, transport, schedule="token-ring",
+                 overlap_steps=True):
+    ctx = mp.get_context("spawn")
+    q_out = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker,
+                         args=(r, world, port, S, H, D, causal, 3, q_out, route, transport, 1,
+                               schedule, overlap_steps))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    _reap.extend(procs)
+    res = {}
+    for _ in range(world):
+        r, calls_out = q_out.get(timeout=300)
+        res[r] = calls_out
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world,S,H,causal,route,transport,schedule", [
+    (4, 4096, 8, True, "ring", "fused", "token-ring"),
+    (4, 4096, 8, True, "ring", "ipc", "token-ring"),
+    (8, 8192, 4, True, "direct", "fused", "token-ring"),
+    (4, 4096, 8, True, "ring", "fused", "ring")])
+def test_overlapped_steps_bit_identical(world, S, H, causal, route, transport, schedule):
+    """Step launches as programmatic dependents of the previous step
+    (overlap_steps, the default) give exactly the results of plain
+    stream-ordered step launches: same kernels, same inputs, only the CTA
+    start times differ."""
+    a = _run_workers(world, S, H, 128, causal, route, transport, schedule, overlap_steps=False)
+    b = _run_workers(world, S, H, 128, causal, route, transport, schedule, overlap_steps=True)
+    for r in range(world):
+        for (oa, la), (ob, lb) in zip(a[r], b[r]):
+            assert np.array_equal(oa, ob) and np.array_equal(la, lb), r
 
 
 def _worker_full(rank, world, port, S, H, D, q_out):
