@@ -498,7 +498,9 @@ def exchange_report(world, runner, xsum, n_fwd, shared):
            "q_bytes_per_forward": q_b / fwd, "out_bytes_per_forward": o_b / fwd,
            "q_gbs": q_b / (q_ms * 1e-3) / 1e9 if q_ms > 0 else None,
            "out_gbs": o_b / (o_ms * 1e-3) / 1e9 if o_ms > 0 else None,
-           "transport": runner.transport}
+           "transport": runner.transport,
+           # ipc / fused: step launches are programmatic dependents of the previous step
+           "overlapped_steps": bool(runner.overlap_steps and runner.transport in ("ipc", "fused"))}
     if k_b > 0:
         rep["kv_bytes_per_forward"] = k_b / fwd
         rep["kv_gbs"] = k_b / (k_ms * 1e-3) / 1e9 if k_ms > 0 else None

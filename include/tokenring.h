@@ -109,7 +109,7 @@ int tr_attention_segments_push_rel(const void* q, const void* k, const void* v, 
                                    uint64_t* done_flag, const int64_t* done_epoch,
                                    int64_t done_offset, void* stream);
 
-/* Launch option of the calling thread's later D=128 attention launches
+/* Launch option of the calling thread's later D=64/128 attention launches
  * (tr_attention_block / _segments / _segments_push*): when on, each is a
  * programmatic dependent launch of the previous kernel on its stream, so its
  * CTAs start on the SMs the previous grid's last wave frees instead of after

@@ -88,6 +88,8 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int ntiles = __shfl_sync(
       0xffffffffu, static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]), 0);
+  // resident: lets a programmatic dependent launch start on freed SMs (no-op otherwise)
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Register rebalancing: each role's code sits inside the branch of its own
   // setmaxnreg so ptxas compiles it against that budget.
@@ -449,8 +451,10 @@ static int launch_d(const void* q, const void* k, const void* v, int64_t tq_tota
   const int vrc = launch_attn_variant(tq, tk, tv, plan, D, blocks, s);
   if (vrc != -1) return vrc;
 #endif
-  attn_fwd_sm100_kernel<D><<<static_cast<unsigned>(blocks), C::THREADS, C::SMEM, s>>>(tq, tk, tv, plan);
-  return cuda_status(cudaGetLastError(), "attn_fwd_sm100 launch");
+  return cuda_status(launch_kernel(attn_fwd_sm100_kernel<D>, dim3(static_cast<unsigned>(blocks)),
+                                   dim3(C::THREADS), C::SMEM, s, plan.overlap_prev != 0, tq, tk,
+                                   tv, plan),
+                     "attn_fwd_sm100 launch");
 }
 
 

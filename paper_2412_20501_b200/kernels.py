@@ -177,8 +177,8 @@ def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shif
 
 
 class overlap_launches:
-    """Context manager: the D=128 attention launches made inside it (this
-    thread) are programmatic dependent launches of the previous kernel on
+    """Context manager: the D=64/128 attention launches and flag waits/sets
+    made inside it (this thread) are programmatic dependent launches of the previous kernel on
     their stream -- their CTAs take the SMs the previous grid's last wave
     frees instead of waiting for the whole grid (tr_set_launch_overlap).
     Only for launches that read nothing the previous kernel writes, e.g.

@@ -233,6 +233,11 @@ class TokenRingAttention:
     ``q_loc/k_loc/v_loc``: this rank's (S/P, H, D) bf16 shard -- its partition
     ranges concatenated in start order (``partition.gather_local``).
     Returns a float32 Partial over the same rows.
+
+    ``overlap_steps`` (ipc / fused): each step's message waits and attention
+    launch are programmatic dependent launches of the previous step, so its
+    CTAs start on the SMs the previous step's last wave frees; results are
+    bit-identical to plain stream-ordered steps (``overlap_steps=False``).
     """
 
     def __init__(self, seq_len, heads, head_dim, causal=True, group=None, ops=None,
