@@ -109,18 +109,25 @@ int tr_attention_segments_push_rel(const void* q, const void* k, const void* v, 
                                    uint64_t* done_flag, const int64_t* done_epoch,
                                    int64_t done_offset, void* stream);
 
-/* Launch option of the calling thread's later D=64/128 attention launches
- * (tr_attention_block / _segments / _segments_push*): when on, each is a
- * programmatic dependent launch of the previous kernel on its stream, so its
- * CTAs start on the SMs the previous grid's last wave frees instead of after
- * the whole grid (the attention kernel triggers its dependents as soon as all
- * of its CTAs are resident).  The launch does not wait for the previous
- * kernel's results: only for a TokenRing step whose inputs were complete
- * before that kernel (every message it reads was waited for by an earlier
- * kernel).  Returns the previous setting; off by default.  No counterpart in
- * the reference, whose steps run one after another on the host
- * (engine.py:468-638). */
-int32_t tr_set_launch_overlap(int32_t on);
+/* Launch options of the calling thread's later D=64/128 attention launches
+ * (tr_attention_block / _segments / _segments_push*), flag-wait and flag-set
+ * launches; flags, 0 (the default) = plain stream-ordered launches:
+ *   TR_LAUNCH_AFTER_PREV   the launch is a programmatic dependent of the
+ *                          previous kernel on its stream: its CTAs start on
+ *                          the SMs the previous grid's last wave frees instead
+ *                          of after the whole grid.  It does not wait for the
+ *                          previous kernel's results -- only for a TokenRing
+ *                          step every message of which was waited for by an
+ *                          earlier kernel.
+ *   TR_LAUNCH_RELEASE_NEXT an attention launch releases its programmatic
+ *                          dependent as soon as all of its CTAs are resident
+ *                          (griddepcontrol.launch_dependents; without it the
+ *                          dependent starts when the grid ends).
+ * Returns the previous flags.  No counterpart in the reference, whose steps
+ * run one after another on the host (engine.py:468-638). */
+#define TR_LAUNCH_AFTER_PREV 1
+#define TR_LAUNCH_RELEASE_NEXT 2
+int32_t tr_set_launch_overlap(int32_t flags);
 
 /* kernels.merge_state, in place on a float32 accumulator:
  *   acc <- merge(acc, blk)     (ref _kernels.pyx:68-102)

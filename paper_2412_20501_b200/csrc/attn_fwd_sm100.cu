@@ -88,8 +88,8 @@ attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_cons
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const int ntiles = __shfl_sync(
       0xffffffffu, static_cast<int>(kv_tiles[0] + kv_tiles[1] + kv_tiles[2] + kv_tiles[3]), 0);
-  // resident: lets a programmatic dependent launch start on freed SMs (no-op otherwise)
-  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // resident: lets a programmatic dependent launch start on freed SMs (TR_LAUNCH_RELEASE_NEXT)
+  if (p.release_next && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Register rebalancing: each role's code sits inside the branch of its own
   // setmaxnreg so ptxas compiles it against that budget.

@@ -19,7 +19,8 @@ static thread_local std::string g_last_error;
 static thread_local int32_t g_launch_overlap = 0;   // tr_set_launch_overlap
 
 void set_error(const std::string& msg) { g_last_error = msg; }
-bool launch_overlap() { return g_launch_overlap != 0; }
+bool launch_overlap() { return (g_launch_overlap & TR_LAUNCH_AFTER_PREV) != 0; }
+bool launch_release_next() { return (g_launch_overlap & TR_LAUNCH_RELEASE_NEXT) != 0; }
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
@@ -162,6 +163,7 @@ static int run_segments(const void* q, const void* k, const void* v, void* out, 
   plan.done_value = push.done_value;
   plan.done_epoch = push.done_epoch;
   plan.overlap_prev = launch_overlap() ? 1 : 0;
+  plan.release_next = launch_release_next() ? 1 : 0;
   plan.tile_prefix[0] = 0;
   for (int i = 0; i < plan.nq; ++i)
     plan.tile_prefix[i + 1] = plan.tile_prefix[i] + (plan.q[i].rows + 255) / 256;
@@ -364,9 +366,9 @@ int tr_enable_peer_access(int32_t peer_device) {
 
 int tr_poll_error(void) { return poll_flag_error(); }
 
-int32_t tr_set_launch_overlap(int32_t on) {
+int32_t tr_set_launch_overlap(int32_t flags) {
   const int32_t prev = g_launch_overlap;
-  g_launch_overlap = on ? 1 : 0;
+  g_launch_overlap = flags & (TR_LAUNCH_AFTER_PREV | TR_LAUNCH_RELEASE_NEXT);
   return prev;
 }
 void tr_clear_error(void) { clear_flag_error(); }

@@ -48,9 +48,13 @@ struct AttnPlan {
   // plain order (head-major, each causal segment heaviest tile first).
   int32_t n_order;
   int32_t head_group;
-  // host side: launch as a programmatic dependent of the previous kernel on
-  // the stream (tr_set_launch_overlap); the kernel itself never waits on it
+  // tr_set_launch_overlap: launch as a programmatic dependent of the previous
+  // kernel on the stream (host side; the kernel never waits on it), and let
+  // the next launch start once every CTA of this one is resident (device:
+  // griddepcontrol.launch_dependents -- only when asked, it is not free:
+  // -0.5..0.9 % sustained when executed by every plain launch)
   int32_t overlap_prev;
+  int32_t release_next;
   uint16_t order[TR_ORDER_MAX];
 };
 
@@ -86,6 +90,7 @@ void set_flag_timeout_ns(unsigned long long ns);
 // and flag-set launches become programmatic dependents of the previous
 // kernel on their stream
 bool launch_overlap();
+bool launch_release_next();
 
 // kernel<<<grid, block, smem, s>>>(args...), or the same as a programmatic
 // dependent launch when `overlap` (cudaLaunchAttributeProgrammaticStreamSerialization)

@@ -176,19 +176,26 @@ def attention_segments_push(q, k, v, q_segs, kv_segs, causal, out, lse, row_shif
     return out, lse
 
 
-class overlap_launches:
-    """Context manager: the D=64/128 attention launches and flag waits/sets
-    made inside it (this thread) are programmatic dependent launches of the previous kernel on
-    their stream -- their CTAs take the SMs the previous grid's last wave
-    frees instead of waiting for the whole grid (tr_set_launch_overlap).
-    Only for launches that read nothing the previous kernel writes, e.g.
-    TokenRing steps whose messages were waited for by an earlier kernel."""
+TR_LAUNCH_AFTER_PREV, TR_LAUNCH_RELEASE_NEXT = 1, 2
 
-    def __init__(self, on=True):
-        self.on = bool(on)
+
+class overlap_launches:
+    """Context manager (tr_set_launch_overlap) for the launches made inside it
+    on this thread.  ``after_prev``: the D=64/128 attention launches and flag
+    waits/sets are programmatic dependent launches of the previous kernel on
+    their stream -- their CTAs take the SMs the previous grid's last wave
+    frees instead of waiting for the whole grid; only for launches that read
+    nothing the previous kernel writes (TokenRing steps whose messages were
+    waited for by an earlier kernel).  ``release_next``: the attention
+    launches let such a dependent start as soon as all their CTAs are
+    resident (otherwise it starts when the grid ends)."""
+
+    def __init__(self, after_prev=True, release_next=True):
+        self.flags = ((TR_LAUNCH_AFTER_PREV if after_prev else 0)
+                      | (TR_LAUNCH_RELEASE_NEXT if release_next else 0))
 
     def __enter__(self):
-        self.prev = _lib.lib().tr_set_launch_overlap(1 if self.on else 0)
+        self.prev = _lib.lib().tr_set_launch_overlap(self.flags)
         return self
 
     def __exit__(self, *exc):

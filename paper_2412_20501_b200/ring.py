@@ -502,7 +502,9 @@ class TokenRingAttention:
             if self.record_timeline:
                 ev["start"] = self.ops.event()
                 self.ops.record(ev["start"])
-            overlap = kernels.overlap_launches(self.overlap_steps and i >= 1)
+            # step i >= 1 after step i-1; every step releases the next one
+            overlap = kernels.overlap_launches(after_prev=self.overlap_steps and i >= 1,
+                                               release_next=self.overlap_steps)
             with overlap:
                 if i >= 1 and (st.q_ids or st.send_q):
                     for src, _ in self.prog[i - 1].recv_q:              # Q_i has landed
@@ -577,8 +579,9 @@ class TokenRingAttention:
                     ev["attn_start"] = self.ops.event()
                     self.ops.record(ev["attn_start"])
                 if i == 0 and self.direct_first:
-                    self.ops.attention(cur_q, kst, vst, q_segs, kv_segs, self.causal,
-                                       self.acc_out, self.acc_lse)
+                    with overlap:
+                        self.ops.attention(cur_q, kst, vst, q_segs, kv_segs, self.causal,
+                                           self.acc_out, self.acc_lse)
                 elif fused and i in fp.push:
                     # compute + send in one kernel: rows go straight into the
                     # home's receive slot over NVLink; its last CTA raises the

@@ -52,7 +52,7 @@ def run_chain(q, k, v, steps, outs, causal, mode, flag):
     overlap = mode != "plain"
     for i, (qs, ks, _) in enumerate(steps):
         o, l = outs[i]
-        with kernels.overlap_launches(overlap and i > 0):
+        with kernels.overlap_launches(after_prev=overlap and i > 0, release_next=overlap):
             if i > 0 and "event" in mode:        # what the runner records between steps
                 torch.cuda.Event().record()
             if i > 0 and "flagwait" in mode:     # an already satisfied message wait

@@ -41,10 +41,11 @@ def main():
     trials = 10
 
     def chain(with_b, overlap):
-        kernels.attention_block(qa, k, v, kernels.MASK_NONE, out=outA, lse=lseA)       # A
+        with kernels.overlap_launches(after_prev=False, release_next=overlap):
+            kernels.attention_block(qa, k, v, kernels.MASK_NONE, out=outA, lse=lseA)   # A
         eA.record()
         if with_b:
-            with kernels.overlap_launches(overlap):
+            with kernels.overlap_launches(after_prev=overlap):
                 kernels.attention_block(qs, ks, vs, kernels.MASK_NONE, out=outB, lse=lseB)  # B
         eB.record()
 
