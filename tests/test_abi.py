@@ -85,6 +85,25 @@ def test_product_library_has_no_runtime_switches(lib):
         assert switch not in strings, switch
 
 
+def test_launch_overlap_flags(lib):
+    """tr_set_launch_overlap: thread-local flags, returns the previous ones,
+    keeps only TR_LAUNCH_AFTER_PREV | TR_LAUNCH_RELEASE_NEXT; off by default
+    (no GPU work)."""
+    from paper_2412_20501_b200 import kernels
+    L = lib.lib()
+    assert L.tr_set_launch_overlap(3) == 0
+    assert L.tr_set_launch_overlap(0xFF) == 3
+    assert L.tr_set_launch_overlap(0) == 3
+    with kernels.overlap_launches(after_prev=False):
+        assert L.tr_set_launch_overlap(kernels.TR_LAUNCH_RELEASE_NEXT) == 2
+    assert L.tr_set_launch_overlap(0) == 0
+    with kernels.overlap_launches():
+        with kernels.overlap_launches(after_prev=True, release_next=False):
+            assert L.tr_set_launch_overlap(1) == 1
+        assert L.tr_set_launch_overlap(3) == 3
+    assert L.tr_set_launch_overlap(0) == 0
+
+
 def test_validation_maps_to_reference_errors(lib):
     from paper_2412_20501_b200.errors import ConfigError, DimensionError
     L = lib.lib()
