@@ -72,6 +72,9 @@ def parse():
                          "IPC-mapped buffer, OUT rows stored by the attention epilogue straight "
                          "into the home rank's receive slot), ipc (copy engines both ways) or "
                          "nccl (torch.distributed P2P, the baseline)")
+    ap.add_argument("--no-overlap-steps", dest="overlap_steps", action="store_false",
+                    help="N>1 ipc/fused: plain stream-ordered step launches instead of "
+                         "programmatic dependent launches of the previous step (A/B)")
     return ap.parse_args()
 
 
@@ -569,7 +572,8 @@ def run_ours(a):
             transport = "nccl"
     causal = not a.non_causal
     runner = TokenRingAttention(S, H, D, causal=causal, record_timeline=True,
-                                transport=transport, schedule=a.schedule)
+                                transport=transport, schedule=a.schedule,
+                                overlap_steps=a.overlap_steps)
     runners = [runner]
     q, k, v = rng.local_inputs(a.seed, runner.part, rank, H, D)
     total_flops = workload_flops(a)
@@ -708,7 +712,7 @@ def run_ours(a):
                       and (g == 1 or ctas_per_head * (H // g) >= 7 * 148))
         def make_runner(hg):
             runners.append(TokenRingAttention(S, hg, D, causal=causal, transport=transport,
-                                              schedule=a.schedule))
+                                              schedule=a.schedule, overlap_steps=a.overlap_steps))
             return runners[-1]
         # the run's first and last groups split off a quarter-size piece, so the
         # exposed pipeline fill / drain is a quarter of a group's copy
